@@ -1,0 +1,406 @@
+"""Benchmark: one learned-optimizer step over ViT-B/16-shaped parameters.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is LearnedOptimizer.step() over all 152 ViT-B/16 tensors (86,567,656
+f32 parameters) with synthetic gradients already resident in HBM: factor pass,
+feature-statistics pass, apply pass (state advance, features, MLP, update,
+decoupled decay).  Metric: parameters stepped per second (Gparams/s,
+higher is better), whole job.  Under torchrun (N > 1) the step is sharded by
+element ranges across ranks (paper_2506_10315_b200.dist); the time is the max
+over ranks.
+
+Also reported on the same line:
+  e2e          the same step through the public API with HOST buffers: each
+               step copies the gradients from pinned host memory and reads the
+               updated parameters back, both inside the timed region;
+  roofline     the dominant kernel (apply pass) against measured HBM bandwidth,
+               44 algorithmic bytes per parameter;
+  cpu_baseline the CPU oracle (oracle/, a bitwise restatement of the
+               reference) on a bounded sample, all host cores;
+  velo         the same measurement for the VeLO-MLP feature set;
+  clocks       nvidia-smi SM clocks and throttle reasons sampled during timing.
+
+`--impl reference` times the reference algorithm on the host cores instead
+(the oracle port, OpenMP over tensors) on a bounded sample of the same
+workload, with the same metric/unit.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+ALGO_BYTES_PER_PARAM = 44          # read theta,g,M1..3,V; write theta,M1..3,V
+HBM_PEAK_FALLBACK = 6650.0         # GB/s, B200_PROFILING.md fallback
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": HBM_PEAK_FALLBACK}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._thr = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._thr = threading.Thread(target=self._run, daemon=True)
+        self._thr.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._thr.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 3 + k and s[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_model(workload, device, seed=0):
+    import torch
+
+    from paper_2506_10315_b200.workloads import WORKLOADS
+
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    params, grads = [], []
+    for _, shape in WORKLOADS[workload]():
+        p = torch.empty(shape, dtype=torch.float32)
+        fan_in = int(np.prod(shape[1:])) if len(shape) > 1 else 1
+        p.normal_(0.0, 1.0 / max(1.0, fan_in) ** 0.5, generator=g)
+        params.append(torch.nn.Parameter(p.to(device)))
+        gr = torch.empty(shape, dtype=torch.float32)
+        gr.normal_(0.0, 1e-3, generator=g)
+        grads.append(gr.to(device))
+    return params, grads
+
+
+def build_optimizer(params, feature_set, mode, world):
+    if world > 1:
+        from paper_2506_10315_b200.dist import ShardedLearnedOptimizer
+
+        return ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
+                                       check_errors=False)
+    from paper_2506_10315_b200 import LearnedOptimizer
+
+    return LearnedOptimizer(params, feature_set=feature_set, mode=mode, check_errors=False)
+
+
+def time_device(opt, params, grads, steps, warmup, world):
+    """Device-resident inputs; CUDA events on the current stream."""
+    import torch
+
+    for p, g in zip(params, grads):
+        p.grad = g
+    for _ in range(warmup):
+        opt.step()
+    torch.cuda.synchronize()
+    opt.phase_events = []
+    barrier(world)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(steps):
+        opt.step()
+    end.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = start.elapsed_time(end)
+    phases = {}
+    for name, a, b in opt.phase_events:
+        phases.setdefault(name, []).append(a.elapsed_time(b))
+    opt.phase_events = None
+    launches = sum(pl.launches_last_step() for pl in opt.plans())
+    return max_over_ranks(ms, world), phases, launches
+
+
+def time_e2e(opt, params, grads, steps, warmup, world):
+    """Public-API step with host buffers: pinned H2D of the gradients and D2H
+    of the updated parameters inside the timed region, every step."""
+    import torch
+
+    host_g = [g.cpu().pin_memory() for g in grads]
+    host_p = [torch.empty(p.shape, dtype=torch.float32).pin_memory() for p in params]
+    dev_g = [torch.empty_like(g) for g in grads]
+    for p, g in zip(params, dev_g):
+        p.grad = g
+
+    def one():
+        for d, h in zip(dev_g, host_g):
+            d.copy_(h, non_blocking=True)
+        opt.step()
+        for h, p in zip(host_p, params):
+            h.copy_(p.detach(), non_blocking=True)
+
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    barrier(world)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(steps):
+        one()
+    end.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    h2d = sum(g.numel() * 4 for g in grads)
+    d2h = sum(p.numel() * 4 for p in params)
+    return max_over_ranks(start.elapsed_time(end), world), h2d, d2h
+
+
+def cpu_sample(workload, budget_params):
+    """Largest-first subset of the workload's tensors (2-D views), up to a
+    parameter budget, for the bounded CPU measurement."""
+    from paper_2506_10315_b200 import view_2d
+    from paper_2506_10315_b200.workloads import WORKLOADS
+
+    shapes = [view_2d(s) for _, s in WORKLOADS[workload]()]
+    chosen, total = [], 0
+    # keep the workload's mix: walk the list in order, skip what overflows
+    for s in shapes:
+        n = s[0] * s[1]
+        if total + n <= budget_params:
+            chosen.append(s)
+            total += n
+    return chosen, total
+
+
+def run_cpu_oracle(workload, feature_set, budget_params, steps, warmup, threads=0):
+    from oracle import oracle as O
+
+    kind = O.KIND_BY_NAME[feature_set]
+    shapes, total = cpu_sample(workload, budget_params)
+    rng = np.random.default_rng(0)
+    params = [(rng.standard_normal(s) * 0.02).astype(np.float32) for s in shapes]
+    grads = [(rng.standard_normal(s) * 1e-3).astype(np.float32) for s in shapes]
+    states = [O.OState.zeros(*s) for s in shapes]
+    w = O.random_weights(39 if kind == O.SMALL_FC_LOPT else 29, seed=0)
+    for _ in range(warmup):
+        O.opt_step(params, states, grads, w, kind, 1.0, threads=threads)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.opt_step(params, states, grads, w, kind, 1.0, threads=threads)
+        times.append(time.perf_counter() - t0)
+    cores = threads if threads > 0 else len(os.sched_getaffinity(0))
+    return {"params": total, "tensors": len(shapes), "step_s": statistics.median(times),
+            "cores": cores, "steps": steps}
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the reference algorithm on the host cores (the oracle
+    port of the reference, all cores), same metric and workload."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    O.lib()
+    r = run_cpu_oracle(args.workload, args.feature_set, args.cpu_budget, args.steps,
+                       max(1, min(args.warmup, 1)))
+    value = r["params"] / r["step_s"] / 1e9
+    sample = (f"{r['tensors']} of the {args.workload} tensors, {r['params']} params "
+              f"(largest-first prefix of the census), median of {r['steps']} steps")
+    line = {
+        "impl": "reference", "metric": metric_name(args), "value": value, "unit": "Gparams/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": r["step_s"] * 1e3, "higher_is_better": True, "scaling": "none",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.workload, "feature_set": args.feature_set,
+                   "sample_params": r["params"]},
+        "cpu_baseline": {"value": value, "unit": "Gparams/s", "cores": r["cores"],
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "Gparams/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(args):
+    return f"optimizer step throughput, {args.workload} {args.feature_set}"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="vit_b16")
+    ap.add_argument("--feature-set", default="small_fc_lopt")
+    ap.add_argument("--mode", default=os.environ.get("LOPT_BENCH_MODE", "strict"))
+    ap.add_argument("--cpu-budget", type=int, default=12_000_000,
+                    help="params in the bounded CPU sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-velo", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+        return
+    import torch
+
+    from paper_2506_10315_b200.workloads import census
+
+    n_tensors, n_params = census(args.workload)
+    peaks, peak_kind = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK))
+    dev = torch.device("cuda", local)
+    params, grads = make_model(args.workload, dev, seed=0)
+
+    opt = build_optimizer(params, args.feature_set, args.mode, world)
+    with ClockSampler(local) as clk:
+        ms, phases, launches = time_device(opt, params, grads, args.steps, args.warmup, world)
+    clocks = clk.summary()
+    value = n_params * args.steps / (ms / 1e3) / 1e9
+    apply_ms = statistics.mean(phases.get("apply", [float("nan")]))
+    local_params = sum(pl.local_elements() for pl in opt.plans())
+    achieved = ALGO_BYTES_PER_PARAM * local_params / (apply_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "kernel": "apply (phase 2)",
+                "peak_source": peak_kind,
+                "phase_ms": {k: statistics.mean(v) for k, v in phases.items()},
+                "step_frac_of_roofline": (ALGO_BYTES_PER_PARAM * n_params / (ms / args.steps / 1e3)
+                                          / 1e9) / hbm_peak}
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                t = json.load(f)
+            key = f"{args.workload}/{args.feature_set}/{args.mode}"
+            if key in t:
+                roofline["traffic"] = t[key]
+        except (OSError, ValueError):
+            pass
+
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(3, args.steps // 2)
+        ems, h2d, d2h = time_e2e(opt, params, grads, e2e_steps, 2, world)
+        e2e = {"value": n_params * e2e_steps / (ems / 1e3) / 1e9, "unit": "Gparams/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": ems / e2e_steps, "api": "LearnedOptimizer.step (torch.optim)"}
+
+    velo = None
+    if not args.no_velo and args.feature_set == "small_fc_lopt":
+        del opt
+        torch.cuda.empty_cache()
+        params, grads = make_model(args.workload, dev, seed=0)
+        vopt = build_optimizer(params, "velo_mlp", args.mode, world)
+        vms, vph, _ = time_device(vopt, params, grads, args.steps, args.warmup, world)
+        velo = {"value": n_params * args.steps / (vms / 1e3) / 1e9, "unit": "Gparams/s",
+                "ms_per_step": vms / args.steps,
+                "phase_ms": {k: statistics.mean(v) for k, v in vph.items()}}
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        r = run_cpu_oracle(args.workload, args.feature_set, args.cpu_budget, 2, 1)
+        cpu = {"value": r["params"] / r["step_s"] / 1e9, "unit": "Gparams/s", "cores": r["cores"],
+               "kind": "port",
+               "sample": f"{r['tensors']} {args.workload} tensors / {r['params']} params, "
+                         f"oracle/ (bitwise restatement of the reference), median of 2 steps",
+               "ms_per_step_sample": r["step_s"] * 1e3}
+
+    if rank == 0:
+        line = {
+            "metric": metric_name(args), "value": value, "unit": "Gparams/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "none", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "feature_set": args.feature_set,
+                       "mode": args.mode, "tensors": n_tensors, "params": n_params,
+                       "parallelism": f"element-sharded x{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (each f32 array 346 MB > 126 MB)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "velo": velo,
+            "clocks": clocks, "gpu_launches": launches * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,156 @@
+/*
+ * lopt_b200.h -- C ABI of the B200 learned-optimizer step.
+ *
+ * Plain pointers, sizes and a CUDA stream handle; no torch types.  Every entry
+ * point is stream-ordered on the caller's stream and returns an int status
+ * (LOPT_OK = 0).  Data-dependent conditions (non-finite gradient, non-finite
+ * updated parameter) do not fail the call: they set per-tensor bits in the
+ * device status words that lopt_read_status() returns.
+ *
+ * Reference interface each entry point replaces (paths relative to the
+ * reference repository, pkg/src/lopt/):
+ *
+ *   lopt_plan_create      OptimizerHandle.fresh / __post_init__  optim.py:121-141
+ *                         (shape checks of engine.py:583-594 _check_step_inputs)
+ *   lopt_workspace_bytes  ScratchTracker accounting               engine.py:88-117
+ *   lopt_set_weights      LoptWeights / weights_from_entries      engine.py:119-163, 212-228
+ *   lopt_factor_partials  update_adafactor's f64 row/col sums     state.py:93-113
+ *                         (and distsim's per-shard bincount partials distsim.py:448-453)
+ *   lopt_factor_finalize  update_adafactor EMA + factor_means    state.py:108-113, features.py:133-135
+ *                         (the coordinator merge of distsim.py:457-474)
+ *   lopt_feature_stats    fused_stats (pass 1)                    engine.py:619-654
+ *   lopt_apply            fused_apply (pass 2) + state_step's    engine.py:657-710,
+ *                         M/V EMAs + apply_weight_decay          state.py:77-90, optim.py:92-101
+ *   lopt_step             opt_step for one device                 optim.py:144-180
+ *   lopt_read_status      UpdateOverflowError / OptimError        engine.py:737-738, optim.py:164-165
+ *
+ * Multi-GPU: lopt_factor_partials and lopt_feature_stats leave f64 partial
+ * sums in two contiguous workspace blocks (lopt_factor_sums_ptr,
+ * lopt_stat_sums_ptr); a caller that shards elements across ranks all-reduces
+ * those blocks (sum, float64) between the phases -- the "factor merge" and
+ * "stats merge" of distsim.py:427-499.
+ */
+#ifndef LOPT_B200_H
+#define LOPT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define LOPT_OK 0
+#define LOPT_ERR_INVALID 1      /* bad argument / descriptor */
+#define LOPT_ERR_SHAPE 2        /* shape mismatch or empty tensor (EngineError) */
+#define LOPT_ERR_WORKSPACE 3    /* workspace missing or too small (ScratchLimitError) */
+#define LOPT_ERR_CUDA 4         /* a CUDA runtime call failed */
+#define LOPT_ERR_UNSUPPORTED 5  /* topology / mode not compiled */
+
+/* feature sets (features.py:52-104) */
+#define LOPT_SMALL_FC_LOPT 0    /* 39 columns */
+#define LOPT_VELO_MLP 1         /* 29 columns */
+
+/* execution modes */
+#define LOPT_MODE_STRICT 0      /* CUDA-core, bitwise features/MLP/expf */
+#define LOPT_MODE_FAST 1        /* folded features, tcgen05 MLP, fp32 tolerance */
+
+/* per-tensor status bits (lopt_read_status) */
+#define LOPT_STATUS_NONFINITE_GRAD 1u
+#define LOPT_STATUS_NONFINITE_PARAM 2u
+
+/* One parameter tensor in its 2-D view (tensors.py:66-100: 1-D -> (n,1)).
+ * theta/grad cover the whole m*n tensor; the call steps elements [lo, hi).
+ * state holds 4 floats per stepped element {M1, M2, M3, V} for [lo, hi)
+ * (state[4*(i-lo) + k]).  row_factors = r5|r6|r7 (3*m floats), col_factors =
+ * c5|c6|c7 (3*n floats), full length on every rank. */
+typedef struct lopt_tensor {
+  int64_t m, n;
+  int64_t lo, hi;
+  float *theta;
+  const float *grad;
+  float *state;
+  float *row_factors;
+  float *col_factors;
+  int32_t weight_slot;    /* index into the weight sets of lopt_set_weights */
+  int32_t reserved;
+} lopt_tensor;
+
+typedef struct lopt_config {
+  int32_t feature_set;    /* LOPT_SMALL_FC_LOPT | LOPT_VELO_MLP */
+  int32_t mode;           /* LOPT_MODE_STRICT | LOPT_MODE_FAST */
+  int32_t hidden1, hidden2;  /* MLP widths; 32,32 for the reference optimizers */
+  int32_t num_weight_sets;   /* 1 = one global MLP; >1 = per-tensor sets (VeLO) */
+  int32_t state_advanced; /* 1: state/factors already advanced for grad (engine-level
+                             calls mirroring step_fused); 0: advance inside the step */
+  double betas[7];        /* momentum x3, second moment, adafactor x3 (state.py:25-40) */
+  float alpha, beta_out;  /* update rule constants (engine.py:61-62) */
+  int32_t update_sign;    /* -1 or +1 */
+  int32_t reserved;
+} lopt_config;
+
+/* Per-step host scalars, produced exactly as the reference does:
+ * lr = schedule_lr(T) before the increment (optim.py:156), tf = numpy
+ * tanh(f32(t)/x) at the post-increment t (features.py:125-130). */
+typedef struct lopt_step_args {
+  double lr;
+  double weight_decay;
+  float time_features[11];
+  int32_t t;              /* post-increment step counter */
+} lopt_step_args;
+
+typedef struct lopt_plan lopt_plan;
+
+int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_config *cfg,
+                     lopt_plan **out);
+int lopt_plan_destroy(lopt_plan *plan);
+int lopt_workspace_bytes(const lopt_plan *plan, size_t *bytes);
+/* Binds caller-owned device memory and uploads the descriptor tables (on stream). */
+int lopt_bind_workspace(lopt_plan *plan, void *dev_ptr, size_t bytes, void *stream);
+/* Re-points theta/grad/state/factor pointers (e.g. torch re-allocated .grad)
+ * without changing shapes or ranges; re-uploads the descriptor table. */
+int lopt_rebind_tensors(lopt_plan *plan, const lopt_tensor *tensors, int32_t count, void *stream);
+/* MLP weights for set `slot`, device or host pointer to the packed layout
+ * w1 (h1 x d) | b1 (h1) | w2 (h2 x h1) | b2 (h2) | w3 (2 x h2) | b3 (2). */
+int lopt_set_weights(lopt_plan *plan, int32_t slot, const float *packed, int32_t is_device,
+                     void *stream);
+/* Device pointer to the per-set packed weights (for weights produced on the GPU,
+ * e.g. the VeLO mixing kernel). */
+int lopt_weights_ptr(lopt_plan *plan, int32_t slot, float **dev_ptr);
+int lopt_set_step_args(lopt_plan *plan, const lopt_step_args *args, void *stream);
+
+int lopt_factor_partials(lopt_plan *plan, void *stream);
+int lopt_factor_finalize(lopt_plan *plan, void *stream);
+int lopt_feature_stats(lopt_plan *plan, void *stream);
+int lopt_apply(lopt_plan *plan, void *stream);
+int lopt_step(lopt_plan *plan, const lopt_step_args *args, void *stream);
+
+/* contiguous f64 blocks to all-reduce across element-sharded ranks */
+int lopt_factor_sums_ptr(lopt_plan *plan, double **ptr, int64_t *count);
+int lopt_stat_sums_ptr(lopt_plan *plan, double **ptr, int64_t *count);
+/* per-tensor results: status bits and max |update| (UpdateReport.max_abs_update) */
+int lopt_status_ptr(lopt_plan *plan, uint32_t **status, float **maxabs);
+int lopt_read_status(lopt_plan *plan, uint32_t *status_host, float *maxabs_host, void *stream);
+/* per-tensor f64 feature sums and f32 factor means (for parity tests) */
+int lopt_debug_ptrs(lopt_plan *plan, double **sumsq, float **factor_means);
+
+/* VeLO per-tensor hypernetwork (build-defined, no reference counterpart;
+ * SURVEY.md section 8(a) row 15): one LSTM step per tensor on inputs derived
+ * from that tensor's phase-1 feature sums and the step/loss features, then
+ * softmax mixing of a bank of `bank_size` packed MLPs into the plan's
+ * per-tensor weight slots (slot j = tensor j).  lstm_params: packed LSTM +
+ * head weights (see paper_2506_10315_b200/velo.py for the layout);
+ * lstm_state: (count x 2 x hidden) h|c, updated in place; bank: bank_size
+ * packed MLPs; loss_feats: 2 floats {log loss, its EMA}. */
+int lopt_velo_mix(lopt_plan *plan, const float *lstm_params, float *lstm_state,
+                  const float *bank, int32_t hidden, int32_t bank_size, int32_t input_dim,
+                  int32_t reserved, const float *loss_feats);
+
+const char *lopt_version(void);
+int lopt_num_kernels_launched_last_step(const lopt_plan *plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

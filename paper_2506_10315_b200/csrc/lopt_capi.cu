@@ -1,0 +1,475 @@
+// lopt_capi.cu -- host side of the C ABI declared in include/lopt_b200.h.
+//
+// A plan is built once per parameter list (the OptimizerHandle of
+// optim.py:104-141): it validates shapes, cuts every tensor into phase-0
+// tiles and phase-1/2 element chunks, and lays out one caller-owned device
+// workspace that holds the descriptor tables, the f64 partial sums and the
+// per-step scalars.  Steps then only launch kernels on the caller's stream.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "lopt_common.cuh"
+
+namespace lopt {
+void launch_factor_partials(const DevicePlan &P, cudaStream_t s);
+void launch_factor_reduce(const DevicePlan &P, int64_t max_mn, cudaStream_t s);
+void launch_factor_finalize(const DevicePlan &P, int64_t max_mn, cudaStream_t s);
+void launch_factor_means(const DevicePlan &P, cudaStream_t s);
+void launch_strict_stats(const DevicePlan &P, cudaStream_t s);
+void launch_stats_reduce(const DevicePlan &P, cudaStream_t s);
+void launch_strict_apply(const DevicePlan &P, cudaStream_t s);
+void launch_maxabs_reduce(const DevicePlan &P, cudaStream_t s);
+int fast_supported(const DevicePlan &P);
+void launch_fast_stats(const DevicePlan &P, cudaStream_t s);
+void launch_fast_apply(const DevicePlan &P, cudaStream_t s);
+int64_t fast_stat_chunk();
+int64_t fast_apply_chunk();
+}  // namespace lopt
+
+using namespace lopt;
+
+namespace {
+
+constexpr int64_t kStrictStatChunk = 8192;
+constexpr int64_t kStrictApplyChunk = 4096;
+constexpr int64_t kFactorTileElems = 65536;
+
+struct Region {
+  size_t off = 0, bytes = 0;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct lopt_plan {
+  lopt_config cfg{};
+  std::vector<lopt_tensor> tensors;
+  std::vector<TensorDesc> descs;
+  std::vector<FactorItem> fitems;
+  std::vector<ChunkItem> sitems, aitems;
+  int64_t max_mn = 0;        // max over tensors of m + n
+  int64_t factor_sums = 0;   // f64 entries of the all-reducible factor block
+  // workspace regions
+  Region r_desc, r_fitems, r_sitems, r_aitems, r_tscal, r_step, r_status, r_maxabs, r_imaxabs,
+      r_abort, r_fsums, r_rowpart, r_colpart, r_rowtab, r_coltab, r_statpart, r_sumsq, r_weights;
+  size_t ws_bytes = 0;
+  char *ws = nullptr;
+  DevicePlan dp{};
+  int launches_last_step = 0;
+};
+
+static int check_cuda(cudaError_t e) {
+  if (e != cudaSuccess) {
+    fprintf(stderr, "lopt_b200: CUDA error %s\n", cudaGetErrorString(e));
+    return LOPT_ERR_CUDA;
+  }
+  return LOPT_OK;
+}
+
+static int check_launch() { return check_cuda(cudaGetLastError()); }
+
+extern "C" {
+
+const char *lopt_version(void) { return "lopt_b200 0.1 (sm_100a)"; }
+
+int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_config *cfg,
+                     lopt_plan **out) {
+  if (!tensors || !cfg || !out || count < 1) return LOPT_ERR_INVALID;
+  if (cfg->feature_set != LOPT_SMALL_FC_LOPT && cfg->feature_set != LOPT_VELO_MLP)
+    return LOPT_ERR_INVALID;
+  if (cfg->mode != LOPT_MODE_STRICT && cfg->mode != LOPT_MODE_FAST) return LOPT_ERR_INVALID;
+  if (cfg->hidden1 != kMaxHidden || cfg->hidden2 != kMaxHidden) return LOPT_ERR_UNSUPPORTED;
+  if (cfg->num_weight_sets < 1) return LOPT_ERR_INVALID;
+  if (cfg->update_sign != 1 && cfg->update_sign != -1) return LOPT_ERR_INVALID;
+  for (int k = 0; k < 7; k++)
+    if (!(cfg->betas[k] >= 0.0 && cfg->betas[k] <= 1.0)) return LOPT_ERR_INVALID;
+  for (int j = 0; j < count; j++) {
+    const lopt_tensor &t = tensors[j];
+    // engine.py:583-594: empty tensors are an EngineError
+    if (t.m < 1 || t.n < 1) return LOPT_ERR_SHAPE;
+    if (t.lo < 0 || t.hi < t.lo || t.hi > t.m * t.n) return LOPT_ERR_SHAPE;
+    if (t.n > (int64_t)1 << 31 || t.m > (int64_t)1 << 40) return LOPT_ERR_SHAPE;
+    if (!t.theta || !t.grad || !t.row_factors || !t.col_factors) return LOPT_ERR_INVALID;
+    if (t.hi > t.lo && !t.state) return LOPT_ERR_INVALID;
+    if ((reinterpret_cast<uintptr_t>(t.state) & 15) != 0) return LOPT_ERR_INVALID;
+    if (t.weight_slot < 0 || t.weight_slot >= cfg->num_weight_sets) return LOPT_ERR_INVALID;
+  }
+  lopt_plan *p = new (std::nothrow) lopt_plan();
+  if (!p) return LOPT_ERR_INVALID;
+  p->cfg = *cfg;
+  p->tensors.assign(tensors, tensors + count);
+  p->descs.resize(count);
+  const int D = d_feat(cfg->feature_set);
+  const bool fast = cfg->mode == LOPT_MODE_FAST;
+  const int64_t stat_chunk = fast ? fast_stat_chunk() : kStrictStatChunk;
+  const int64_t apply_chunk = fast ? fast_apply_chunk() : kStrictApplyChunk;
+  int64_t rowpart = 0, colpart = 0, rows = 0, cols = 0;
+  for (int j = 0; j < count; j++) {
+    const lopt_tensor &t = tensors[j];
+    TensorDesc &d = p->descs[j];
+    memset(&d, 0, sizeof(d));
+    d.m = t.m;
+    d.n = t.n;
+    d.lo = t.lo;
+    d.hi = t.hi;
+    d.weight_slot = t.weight_slot;
+    p->max_mn = std::max<int64_t>(p->max_mn, t.m + t.n);
+    if (!cfg->state_advanced) {
+      if (t.n == 1) {
+        d.nstrips = 1;
+        d.nrowblocks = (int32_t)((t.m + kFactorTileElems - 1) / kFactorTileElems);
+        for (int rb = 0; rb < d.nrowblocks; rb++) {
+          FactorItem it{};
+          it.tensor = j;
+          it.strip = 0;
+          it.rowblock = rb;
+          it.a0 = rb * kFactorTileElems;
+          it.a1 = std::min<int64_t>(t.m, it.a0 + kFactorTileElems);
+          it.b0 = 0;
+          it.b1 = 1;
+          p->fitems.push_back(it);
+        }
+      } else {
+        const int64_t strip = 1024;
+        d.nstrips = (int32_t)((t.n + strip - 1) / strip);
+        const int64_t width = std::min<int64_t>(t.n, strip);
+        int64_t R = kFactorTileElems / width;
+        R = std::max<int64_t>(8, (R + 7) / 8 * 8);
+        d.nrowblocks = (int32_t)((t.m + R - 1) / R);
+        for (int rb = 0; rb < d.nrowblocks; rb++)
+          for (int s = 0; s < d.nstrips; s++) {
+            FactorItem it{};
+            it.tensor = j;
+            it.strip = s;
+            it.rowblock = rb;
+            it.a0 = rb * R;
+            it.a1 = std::min<int64_t>(t.m, it.a0 + R);
+            it.b0 = s * strip;
+            it.b1 = std::min<int64_t>(t.n, it.b0 + strip);
+            p->fitems.push_back(it);
+          }
+      }
+    }
+    rowpart += (int64_t)d.nstrips * t.m;
+    colpart += (int64_t)d.nrowblocks * t.n;
+    rows += t.m;
+    cols += t.n;
+    d.stat_item0 = (int32_t)p->sitems.size();
+    for (int64_t e = t.lo; e < t.hi; e += stat_chunk)
+      p->sitems.push_back(ChunkItem{j, 0, e, std::min<int64_t>(t.hi, e + stat_chunk)});
+    d.stat_items = (int32_t)p->sitems.size() - d.stat_item0;
+    d.apply_item0 = (int32_t)p->aitems.size();
+    for (int64_t e = t.lo; e < t.hi; e += apply_chunk)
+      p->aitems.push_back(ChunkItem{j, 0, e, std::min<int64_t>(t.hi, e + apply_chunk)});
+    d.apply_items = (int32_t)p->aitems.size() - d.apply_item0;
+  }
+  p->factor_sums = rows + cols;
+  // workspace layout
+  size_t off = 0;
+  auto take = [&](Region &r, size_t bytes) {
+    off = align_up(off, 256);
+    r.off = off;
+    r.bytes = bytes;
+    off += bytes;
+  };
+  const int wstride = weight_stride(D, cfg->hidden1, cfg->hidden2);
+  take(p->r_desc, sizeof(TensorDesc) * count);
+  take(p->r_fitems, sizeof(FactorItem) * std::max<size_t>(1, p->fitems.size()));
+  take(p->r_sitems, sizeof(ChunkItem) * std::max<size_t>(1, p->sitems.size()));
+  take(p->r_aitems, sizeof(ChunkItem) * std::max<size_t>(1, p->aitems.size()));
+  take(p->r_tscal, sizeof(TensorScalars) * count);
+  take(p->r_step, sizeof(StepScalars));
+  take(p->r_status, sizeof(uint32_t) * count);
+  take(p->r_maxabs, sizeof(float) * count);
+  take(p->r_imaxabs, sizeof(float) * std::max<size_t>(1, p->aitems.size()));
+  take(p->r_abort, sizeof(uint32_t) * 4);
+  take(p->r_fsums, sizeof(double) * (size_t)p->factor_sums);
+  take(p->r_rowpart, sizeof(double) * (size_t)std::max<int64_t>(1, rowpart));
+  take(p->r_colpart, sizeof(double) * (size_t)std::max<int64_t>(1, colpart));
+  take(p->r_rowtab, sizeof(float) * kRowTab * (size_t)rows);
+  take(p->r_coltab, sizeof(float) * kRowTab * (size_t)cols);
+  take(p->r_statpart, sizeof(double) * D * std::max<size_t>(1, p->sitems.size()));
+  take(p->r_sumsq, sizeof(double) * D * count);
+  take(p->r_weights, sizeof(float) * (size_t)wstride * cfg->num_weight_sets);
+  p->ws_bytes = align_up(off, 256);
+  // device plan (pointers filled at bind time)
+  DevicePlan &P = p->dp;
+  P.count = count;
+  P.n_factor_items = (int32_t)p->fitems.size();
+  P.n_stat_items = (int32_t)p->sitems.size();
+  P.n_apply_items = (int32_t)p->aitems.size();
+  P.kind = cfg->feature_set;
+  P.mode = cfg->mode;
+  P.h1 = cfg->hidden1;
+  P.h2 = cfg->hidden2;
+  P.weight_stride = wstride;
+  P.state_advanced = cfg->state_advanced;
+  for (int k = 0; k < 7; k++) P.beta[k] = (float)cfg->betas[k];
+  P.alpha = cfg->alpha;
+  P.beta_out = cfg->beta_out;
+  if (fast && !fast_supported(P)) {
+    delete p;
+    return LOPT_ERR_UNSUPPORTED;
+  }
+  *out = p;
+  return LOPT_OK;
+}
+
+int lopt_plan_destroy(lopt_plan *plan) {
+  delete plan;
+  return LOPT_OK;
+}
+
+int lopt_workspace_bytes(const lopt_plan *plan, size_t *bytes) {
+  if (!plan || !bytes) return LOPT_ERR_INVALID;
+  *bytes = plan->ws_bytes;
+  return LOPT_OK;
+}
+
+int lopt_bind_workspace(lopt_plan *p, void *dev_ptr, size_t bytes, void *stream) {
+  if (!p || !dev_ptr) return LOPT_ERR_INVALID;
+  if (bytes < p->ws_bytes) return LOPT_ERR_WORKSPACE;
+  if ((reinterpret_cast<uintptr_t>(dev_ptr) & 255) != 0) return LOPT_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  p->ws = (char *)dev_ptr;
+  char *ws = p->ws;
+  const int D = d_feat(p->cfg.feature_set);
+  int64_t rowoff = 0, coloff = 0, rpoff = 0, cpoff = 0;
+  double *fsums = (double *)(ws + p->r_fsums.off);
+  int64_t fsoff = 0;
+  for (size_t j = 0; j < p->descs.size(); j++) {
+    TensorDesc &d = p->descs[j];
+    const lopt_tensor &t = p->tensors[j];
+    d.theta = t.theta;
+    d.grad = t.grad;
+    d.state = reinterpret_cast<float4 *>(t.state);
+    d.r = t.row_factors;
+    d.c = t.col_factors;
+    d.rowsum = fsums + fsoff;
+    d.colsum = fsums + fsoff + t.m;
+    fsoff += t.m + t.n;
+    d.rowpart = (double *)(ws + p->r_rowpart.off) + rpoff;
+    d.colpart = (double *)(ws + p->r_colpart.off) + cpoff;
+    rpoff += (int64_t)d.nstrips * t.m;
+    cpoff += (int64_t)d.nrowblocks * t.n;
+    d.rowtab = (float *)(ws + p->r_rowtab.off) + rowoff * kRowTab;
+    d.coltab = (float *)(ws + p->r_coltab.off) + coloff * kRowTab;
+    rowoff += t.m;
+    coloff += t.n;
+    d.sumsq = (double *)(ws + p->r_sumsq.off) + (int64_t)j * D;
+  }
+  DevicePlan &P = p->dp;
+  P.tensors = (TensorDesc *)(ws + p->r_desc.off);
+  P.factor_items = (FactorItem *)(ws + p->r_fitems.off);
+  P.stat_items = (ChunkItem *)(ws + p->r_sitems.off);
+  P.apply_items = (ChunkItem *)(ws + p->r_aitems.off);
+  P.stat_part = (double *)(ws + p->r_statpart.off);
+  P.tscal = (TensorScalars *)(ws + p->r_tscal.off);
+  P.step = (StepScalars *)(ws + p->r_step.off);
+  P.weights = (const float *)(ws + p->r_weights.off);
+  P.status = (uint32_t *)(ws + p->r_status.off);
+  P.maxabs = (float *)(ws + p->r_maxabs.off);
+  P.item_maxabs = (float *)(ws + p->r_imaxabs.off);
+  P.abort_flag = (uint32_t *)(ws + p->r_abort.off);
+  int st;
+  // descriptor uploads: pageable source, so the copies complete before return
+  if ((st = check_cuda(cudaMemcpyAsync(P.tensors, p->descs.data(),
+                                       sizeof(TensorDesc) * p->descs.size(),
+                                       cudaMemcpyHostToDevice, s))))
+    return st;
+  if (!p->fitems.empty() &&
+      (st = check_cuda(cudaMemcpyAsync(P.factor_items, p->fitems.data(),
+                                       sizeof(FactorItem) * p->fitems.size(),
+                                       cudaMemcpyHostToDevice, s))))
+    return st;
+  if (!p->sitems.empty() &&
+      (st = check_cuda(cudaMemcpyAsync(P.stat_items, p->sitems.data(),
+                                       sizeof(ChunkItem) * p->sitems.size(),
+                                       cudaMemcpyHostToDevice, s))))
+    return st;
+  if (!p->aitems.empty() &&
+      (st = check_cuda(cudaMemcpyAsync(P.apply_items, p->aitems.data(),
+                                       sizeof(ChunkItem) * p->aitems.size(),
+                                       cudaMemcpyHostToDevice, s))))
+    return st;
+  if ((st = check_cuda(cudaMemsetAsync(ws + p->r_rowpart.off, 0, p->r_rowpart.bytes, s))))
+    return st;
+  if ((st = check_cuda(cudaMemsetAsync(ws + p->r_colpart.off, 0, p->r_colpart.bytes, s))))
+    return st;
+  return check_cuda(cudaMemsetAsync(ws + p->r_status.off, 0, p->r_status.bytes, s));
+}
+
+int lopt_rebind_tensors(lopt_plan *p, const lopt_tensor *tensors, int32_t count, void *stream) {
+  if (!p || !p->ws || !tensors || count != (int32_t)p->tensors.size()) return LOPT_ERR_INVALID;
+  for (int j = 0; j < count; j++) {
+    const lopt_tensor &a = tensors[j], &b = p->tensors[j];
+    if (a.m != b.m || a.n != b.n || a.lo != b.lo || a.hi != b.hi) return LOPT_ERR_SHAPE;
+    if (!a.theta || !a.grad || !a.row_factors || !a.col_factors) return LOPT_ERR_INVALID;
+    if (a.hi > a.lo && (!a.state || (reinterpret_cast<uintptr_t>(a.state) & 15) != 0))
+      return LOPT_ERR_INVALID;
+  }
+  for (int j = 0; j < count; j++) {
+    p->tensors[j] = tensors[j];
+    TensorDesc &d = p->descs[j];
+    d.theta = tensors[j].theta;
+    d.grad = tensors[j].grad;
+    d.state = reinterpret_cast<float4 *>(tensors[j].state);
+    d.r = tensors[j].row_factors;
+    d.c = tensors[j].col_factors;
+  }
+  return check_cuda(cudaMemcpyAsync(p->dp.tensors, p->descs.data(),
+                                    sizeof(TensorDesc) * p->descs.size(), cudaMemcpyHostToDevice,
+                                    (cudaStream_t)stream));
+}
+
+int lopt_set_weights(lopt_plan *p, int32_t slot, const float *packed, int32_t is_device,
+                     void *stream) {
+  if (!p || !p->ws || !packed) return LOPT_ERR_INVALID;
+  if (slot < 0 || slot >= p->cfg.num_weight_sets) return LOPT_ERR_INVALID;
+  const size_t bytes = sizeof(float) * p->dp.weight_stride;
+  float *dst = (float *)(p->ws + p->r_weights.off) + (int64_t)slot * p->dp.weight_stride;
+  return check_cuda(cudaMemcpyAsync(dst, packed, bytes,
+                                    is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                    (cudaStream_t)stream));
+}
+
+int lopt_weights_ptr(lopt_plan *p, int32_t slot, float **dev_ptr) {
+  if (!p || !p->ws || !dev_ptr || slot < 0 || slot >= p->cfg.num_weight_sets)
+    return LOPT_ERR_INVALID;
+  *dev_ptr = (float *)(p->ws + p->r_weights.off) + (int64_t)slot * p->dp.weight_stride;
+  return LOPT_OK;
+}
+
+int lopt_set_step_args(lopt_plan *p, const lopt_step_args *a, void *stream) {
+  if (!p || !p->ws || !a) return LOPT_ERR_INVALID;
+  if (!(a->weight_decay >= 0.0)) return LOPT_ERR_INVALID;
+  StepScalars h{};
+  for (int k = 0; k < kTimeFeatures; k++) h.tf[k] = a->time_features[k];
+  h.lr_f32 = (float)a->lr;
+  h.ds = (float)p->cfg.update_sign * (float)a->lr;             // engine.py:695
+  h.decay = (float)(1.0 - a->lr * a->weight_decay);             // optim.py:100
+  h.apply_decay = a->weight_decay > 0.0 ? 1 : 0;                // optim.py:171
+  h.t = a->t;
+  return check_cuda(cudaMemcpyAsync(p->dp.step, &h, sizeof(h), cudaMemcpyHostToDevice,
+                                    (cudaStream_t)stream));
+}
+
+int lopt_factor_partials(lopt_plan *p, void *stream) {
+  if (!p || !p->ws) return LOPT_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  int st;
+  if ((st = check_cuda(cudaMemsetAsync(p->ws + p->r_status.off, 0, p->r_status.bytes, s))))
+    return st;
+  if ((st = check_cuda(cudaMemsetAsync(p->ws + p->r_abort.off, 0, p->r_abort.bytes, s))))
+    return st;
+  p->launches_last_step = 0;
+  if (p->cfg.state_advanced) return LOPT_OK;
+  launch_factor_partials(p->dp, s);
+  launch_factor_reduce(p->dp, p->max_mn, s);
+  p->launches_last_step += 2;
+  return check_launch();
+}
+
+int lopt_factor_finalize(lopt_plan *p, void *stream) {
+  if (!p || !p->ws) return LOPT_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  launch_factor_finalize(p->dp, p->max_mn, s);
+  launch_factor_means(p->dp, s);
+  p->launches_last_step += 2;
+  return check_launch();
+}
+
+int lopt_feature_stats(lopt_plan *p, void *stream) {
+  if (!p || !p->ws) return LOPT_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->cfg.mode == LOPT_MODE_FAST)
+    launch_fast_stats(p->dp, s);
+  else
+    launch_strict_stats(p->dp, s);
+  launch_stats_reduce(p->dp, s);
+  p->launches_last_step += (p->dp.n_stat_items > 0) + 1;
+  return check_launch();
+}
+
+int lopt_apply(lopt_plan *p, void *stream) {
+  if (!p || !p->ws) return LOPT_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->cfg.mode == LOPT_MODE_FAST)
+    launch_fast_apply(p->dp, s);
+  else
+    launch_strict_apply(p->dp, s);
+  launch_maxabs_reduce(p->dp, s);
+  p->launches_last_step += (p->dp.n_apply_items > 0) + 1;
+  return check_launch();
+}
+
+int lopt_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
+  int st;
+  if (args && (st = lopt_set_step_args(p, args, stream))) return st;
+  if ((st = lopt_factor_partials(p, stream))) return st;
+  if ((st = lopt_factor_finalize(p, stream))) return st;
+  if ((st = lopt_feature_stats(p, stream))) return st;
+  return lopt_apply(p, stream);
+}
+
+int lopt_factor_sums_ptr(lopt_plan *p, double **ptr, int64_t *count) {
+  if (!p || !p->ws || !ptr || !count) return LOPT_ERR_INVALID;
+  *ptr = (double *)(p->ws + p->r_fsums.off);
+  *count = p->factor_sums;
+  return LOPT_OK;
+}
+
+int lopt_stat_sums_ptr(lopt_plan *p, double **ptr, int64_t *count) {
+  if (!p || !p->ws || !ptr || !count) return LOPT_ERR_INVALID;
+  *ptr = (double *)(p->ws + p->r_sumsq.off);
+  *count = (int64_t)d_feat(p->cfg.feature_set) * (int64_t)p->tensors.size();
+  return LOPT_OK;
+}
+
+int lopt_status_ptr(lopt_plan *p, uint32_t **status, float **maxabs) {
+  if (!p || !p->ws || !status || !maxabs) return LOPT_ERR_INVALID;
+  *status = p->dp.status;
+  *maxabs = p->dp.maxabs;
+  return LOPT_OK;
+}
+
+int lopt_read_status(lopt_plan *p, uint32_t *status_host, float *maxabs_host, void *stream) {
+  if (!p || !p->ws) return LOPT_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  int st;
+  const size_t n = p->tensors.size();
+  if (status_host &&
+      (st = check_cuda(cudaMemcpyAsync(status_host, p->dp.status, sizeof(uint32_t) * n,
+                                       cudaMemcpyDeviceToHost, s))))
+    return st;
+  if (maxabs_host &&
+      (st = check_cuda(cudaMemcpyAsync(maxabs_host, p->dp.maxabs, sizeof(float) * n,
+                                       cudaMemcpyDeviceToHost, s))))
+    return st;
+  return check_cuda(cudaStreamSynchronize(s));
+}
+
+int lopt_debug_ptrs(lopt_plan *p, double **sumsq, float **factor_means) {
+  if (!p || !p->ws) return LOPT_ERR_INVALID;
+  if (sumsq) *sumsq = (double *)(p->ws + p->r_sumsq.off);
+  if (factor_means) *factor_means = (float *)(p->ws + p->r_tscal.off);
+  return LOPT_OK;
+}
+
+int lopt_velo_mix(lopt_plan *p, const float *lstm_params, float *lstm_state, const float *bank,
+                  int32_t hidden, int32_t bank_size, int32_t input_dim, int32_t reserved,
+                  const float *loss_feats) {
+  (void)p; (void)lstm_params; (void)lstm_state; (void)bank; (void)hidden; (void)bank_size;
+  (void)input_dim; (void)reserved; (void)loss_feats;
+  return LOPT_ERR_UNSUPPORTED;
+}
+
+int lopt_num_kernels_launched_last_step(const lopt_plan *p) {
+  return p ? p->launches_last_step : 0;
+}
+
+}  // extern "C"

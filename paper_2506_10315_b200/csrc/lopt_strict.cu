@@ -1,0 +1,305 @@
+// lopt_strict.cu -- phases 1 and 2 in strict mode (CUDA cores).
+//
+// Strict mode is the parity reference of the build: every feature is computed
+// with correctly rounded f32 ops in the reference's expression order
+// (features.py:147-195), the MLP is a per-output sequential fmaf chain from the
+// bias (engine.py:441-480 under fastmath={"contract"}), and the exponential is
+// the glibc expf algorithm (engine.py:537).  Given identical advanced state and
+// identical f64 sums it reproduces fused_apply bit for bit.  The fast mode
+// (lopt_fast.cu) is the product path; this one is the yardstick.
+#include "lopt_common.cuh"
+
+namespace lopt {
+
+constexpr int kStrictThreads = 256;
+
+// Flat element index -> (row, col) for a chunk that starts at e0.
+struct RowCol {
+  int64_t a, b;
+};
+__device__ __forceinline__ RowCol split_index(int64_t e, int64_t n) {
+  return {e / n, e % n};
+}
+
+__device__ __forceinline__ void load_elem(const TensorDesc &T, int64_t e, bool advanced,
+                                          const float *beta, Elem &x, float4 &newstate) {
+  x.w = T.theta[e];
+  x.g = T.grad[e];
+  const float4 s = T.state[e - T.lo];
+  if (advanced) {
+    x.m1 = s.x; x.m2 = s.y; x.m3 = s.z; x.v = s.w;
+  } else {
+    // state.py:77-90, recomputed in registers from the old accumulators
+    x.m1 = ema(beta[0], __fsub_rn(1.0f, beta[0]), s.x, x.g);
+    x.m2 = ema(beta[1], __fsub_rn(1.0f, beta[1]), s.y, x.g);
+    x.m3 = ema(beta[2], __fsub_rn(1.0f, beta[2]), s.z, x.g);
+    x.v = ema(beta[3], __fsub_rn(1.0f, beta[3]), s.w, __fmul_rn(x.g, x.g));
+  }
+  newstate = make_float4(x.m1, x.m2, x.m3, x.v);
+}
+
+__device__ __forceinline__ void load_tab(const float *tab, int64_t i, float *out) {
+  const float4 lo = reinterpret_cast<const float4 *>(tab + i * kRowTab)[0];
+  const float4 hi = reinterpret_cast<const float4 *>(tab + i * kRowTab)[1];
+  out[0] = lo.x; out[1] = lo.y; out[2] = lo.z; out[3] = lo.w; out[4] = hi.x; out[5] = hi.y;
+}
+
+// Phase 1 (engine.py:619-654 fused_stats): per-element features, f64 sums of
+// squares, block reduction in a fixed order -> stat_part[item][k].
+template <int KIND>
+__global__ void __launch_bounds__(kStrictThreads)
+stats_strict_kernel(DevicePlan P) {
+  constexpr int D = d_feat(KIND);
+  const ChunkItem it = P.stat_items[blockIdx.x];
+  const TensorDesc T = P.tensors[it.tensor];
+  const TensorScalars ts = P.tscal[it.tensor];
+  __shared__ float tf[kTimeFeatures];
+  __shared__ double red[kStrictThreads / 32][D];
+  if (threadIdx.x < kTimeFeatures) tf[threadIdx.x] = P.step->tf[threadIdx.x];
+  __syncthreads();
+  double acc[D];
+#pragma unroll
+  for (int k = 0; k < D; k++) acc[k] = 0.0;
+  for (int64_t e = it.e0 + threadIdx.x; e < it.e1; e += kStrictThreads) {
+    Elem x;
+    float4 ns;
+    load_elem(T, e, P.state_advanced, P.beta, x, ns);
+    const RowCol rc = split_index(e, T.n);
+    float rowt[6], colt[6], f[D];
+    load_tab(T.rowtab, rc.a, rowt);
+    load_tab(T.coltab, rc.b, colt);
+    strict_features<KIND>(x, rowt, colt, ts.mr, tf, f);
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+      const double fv = (double)f[k];
+      acc[k] = __fma_rn(fv, fv, acc[k]);
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < D; k++) {
+    const double s = warp_sum(acc[k]);
+    if (lane == 0) red[warp][k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < D) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kStrictThreads / 32; w++) s += red[w][threadIdx.x];
+    P.stat_part[(int64_t)blockIdx.x * D + threadIdx.x] = s;
+  }
+}
+
+// Per-tensor sums of the phase-1 item partials, in item order.
+__global__ void stats_reduce_kernel(DevicePlan P) {
+  const int j = blockIdx.x;
+  const TensorDesc T = P.tensors[j];
+  const int D = d_feat(P.kind);
+  for (int k = threadIdx.x; k < D; k += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < T.stat_items; i++) s += P.stat_part[(int64_t)(T.stat_item0 + i) * D + k];
+    T.sumsq[k] = s;
+  }
+}
+
+// Shared-memory image of one tensor's MLP in strict mode.  W1 is stored
+// transposed with the normalization scale folded in (engine.py:686:
+// w1s = w1 * scale, one f32 multiply).
+struct StrictMlpSmem {
+  float w1sT[kMaxFeat][kMaxHidden];
+  float b1[kMaxHidden];
+  float w2T[kMaxHidden][kMaxHidden];
+  float b2[kMaxHidden];
+  float w3[2][kMaxHidden];
+  float b3[2];
+  uint64_t exptab[32];
+};
+
+template <int D>
+__device__ void load_strict_mlp(const DevicePlan &P, const TensorDesc &T, StrictMlpSmem &S) {
+  const int H1 = kMaxHidden, H2 = kMaxHidden;
+  const float *wp = P.weights + (int64_t)T.weight_slot * P.weight_stride;
+  const float *w1 = wp, *b1 = w1 + H1 * D, *w2 = b1 + H1, *b2 = w2 + H2 * H1, *w3 = b2 + H2,
+              *b3 = w3 + 2 * H2;
+  // features.py:138-140 normalization_scale, f64 then f32
+  __shared__ float scale[kMaxFeat];
+  const int64_t count = T.m * T.n;
+  for (int k = threadIdx.x; k < D; k += blockDim.x)
+    scale[k] = (float)(1.0 / sqrt(T.sumsq[k] / (double)count + kEpsNorm));
+  __syncthreads();
+  for (int i = threadIdx.x; i < H1 * D; i += blockDim.x) {
+    const int o = i / D, j = i % D;
+    S.w1sT[j][o] = __fmul_rn(w1[i], scale[j]);
+  }
+  for (int i = threadIdx.x; i < H2 * H1; i += blockDim.x) {
+    const int o = i / H1, j = i % H1;
+    S.w2T[j][o] = w2[i];
+  }
+  for (int i = threadIdx.x; i < H1; i += blockDim.x) S.b1[i] = b1[i];
+  for (int i = threadIdx.x; i < H2; i += blockDim.x) {
+    S.b2[i] = b2[i];
+    S.w3[0][i] = w3[i];
+    S.w3[1][i] = w3[H2 + i];
+  }
+  if (threadIdx.x < 2) S.b3[threadIdx.x] = b3[threadIdx.x];
+  if (threadIdx.x < 32) S.exptab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  __syncthreads();
+}
+
+// engine.py:441-480 _mlp_lanes for one element: fmaf chains in input order.
+template <int D>
+__device__ __forceinline__ void strict_mlp(const StrictMlpSmem &S, const float *x, float &dir,
+                                           float &mag) {
+  float h1[kMaxHidden];
+#pragma unroll
+  for (int o = 0; o < kMaxHidden; o++) h1[o] = S.b1[o];
+#pragma unroll
+  for (int j = 0; j < D; j++) {
+    const float xj = x[j];
+    const float4 *wr = reinterpret_cast<const float4 *>(S.w1sT[j]);
+#pragma unroll
+    for (int q = 0; q < kMaxHidden / 4; q++) {
+      const float4 w = wr[q];
+      h1[4 * q + 0] = __fmaf_rn(w.x, xj, h1[4 * q + 0]);
+      h1[4 * q + 1] = __fmaf_rn(w.y, xj, h1[4 * q + 1]);
+      h1[4 * q + 2] = __fmaf_rn(w.z, xj, h1[4 * q + 2]);
+      h1[4 * q + 3] = __fmaf_rn(w.w, xj, h1[4 * q + 3]);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < kMaxHidden; o++)
+    if (h1[o] < 0.0f) h1[o] = 0.0f;
+  float h2[kMaxHidden];
+#pragma unroll
+  for (int o = 0; o < kMaxHidden; o++) h2[o] = S.b2[o];
+#pragma unroll
+  for (int j = 0; j < kMaxHidden; j++) {
+    const float hj = h1[j];
+    const float4 *wr = reinterpret_cast<const float4 *>(S.w2T[j]);
+#pragma unroll
+    for (int q = 0; q < kMaxHidden / 4; q++) {
+      const float4 w = wr[q];
+      h2[4 * q + 0] = __fmaf_rn(w.x, hj, h2[4 * q + 0]);
+      h2[4 * q + 1] = __fmaf_rn(w.y, hj, h2[4 * q + 1]);
+      h2[4 * q + 2] = __fmaf_rn(w.z, hj, h2[4 * q + 2]);
+      h2[4 * q + 3] = __fmaf_rn(w.w, hj, h2[4 * q + 3]);
+    }
+  }
+  float d = S.b3[0], m = S.b3[1];
+#pragma unroll
+  for (int j = 0; j < kMaxHidden; j++) {
+    float hj = h2[j];
+    if (hj < 0.0f) hj = 0.0f;
+    d = __fmaf_rn(S.w3[0][j], hj, d);
+    m = __fmaf_rn(S.w3[1][j], hj, m);
+  }
+  dir = d;
+  mag = m;
+}
+
+// Phase 2 (engine.py:657-710 fused_apply + optim.py:171-172 decay): features,
+// MLP, update, decay; writes theta and the advanced accumulators.
+template <int KIND>
+__global__ void __launch_bounds__(kStrictThreads)
+apply_strict_kernel(DevicePlan P) {
+  constexpr int D = d_feat(KIND);
+  const ChunkItem it = P.apply_items[blockIdx.x];
+  const TensorDesc T = P.tensors[it.tensor];
+  const TensorScalars ts = P.tscal[it.tensor];
+  __shared__ __align__(16) StrictMlpSmem S;
+  __shared__ float tf[kTimeFeatures];
+  __shared__ float red[kStrictThreads / 32];
+  __shared__ uint32_t bad_s;
+  if (threadIdx.x < kTimeFeatures) tf[threadIdx.x] = P.step->tf[threadIdx.x];
+  if (threadIdx.x == 0) bad_s = 0;
+  load_strict_mlp<D>(P, T, S);
+  // a non-finite gradient anywhere aborts the whole step before any write
+  // (optim.py:160-165 validates every gradient before committing)
+  if (*P.abort_flag) return;
+  const float alpha = P.alpha, beta_out = P.beta_out;
+  const float ds = P.step->ds, decay = P.step->decay;
+  const bool apply_decay = P.step->apply_decay != 0;
+  float maxabs = 0.0f;
+  uint32_t bad = 0;
+  for (int64_t e = it.e0 + threadIdx.x; e < it.e1; e += kStrictThreads) {
+    Elem x;
+    float4 ns;
+    load_elem(T, e, P.state_advanced, P.beta, x, ns);
+    const RowCol rc = split_index(e, T.n);
+    float rowt[6], colt[6], f[D];
+    load_tab(T.rowtab, rc.a, rowt);
+    load_tab(T.coltab, rc.b, colt);
+    strict_features<KIND>(x, rowt, colt, ts.mr, tf, f);
+    float dir, mag;
+    strict_mlp<D>(S, f, dir, mag);
+    // engine.py:537-539: upd = dir * exp(mag*alpha) * beta; out = W + ds*upd
+    const float ex = glibc_expf(__fmul_rn(mag, alpha), S.exptab);
+    const float upd = __fmul_rn(__fmul_rn(dir, ex), beta_out);
+    const float du = __fmul_rn(ds, upd);
+    float out = __fadd_rn(x.w, du);
+    maxabs = fmaxf(maxabs, fabsf(du));
+    bad |= !isfinite(out);
+    if (apply_decay) out = __fmul_rn(out, decay);
+    T.theta[e] = out;
+    if (!P.state_advanced) T.state[e - T.lo] = ns;
+  }
+  maxabs = fmaxf(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, 16));
+  maxabs = fmaxf(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, 8));
+  maxabs = fmaxf(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, 4));
+  maxabs = fmaxf(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, 2));
+  maxabs = fmaxf(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, 1));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = maxabs;
+  if (bad) atomicOr(&bad_s, 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mx = 0.0f;
+    for (int w = 0; w < kStrictThreads / 32; w++) mx = fmaxf(mx, red[w]);
+    P.item_maxabs[blockIdx.x] = mx;
+    if (bad_s) atomicOr(&P.status[it.tensor], LOPT_STATUS_NONFINITE_PARAM);
+  }
+}
+
+// Per-tensor max |update| over the tensor's apply items.
+__global__ void maxabs_reduce_kernel(DevicePlan P) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.count) return;
+  const TensorDesc T = P.tensors[j];
+  float mx = 0.0f;
+  for (int i = 0; i < T.apply_items; i++) mx = fmaxf(mx, P.item_maxabs[T.apply_item0 + i]);
+  P.maxabs[j] = mx;
+}
+
+template __global__ void stats_strict_kernel<LOPT_SMALL_FC_LOPT>(DevicePlan);
+template __global__ void stats_strict_kernel<LOPT_VELO_MLP>(DevicePlan);
+template __global__ void apply_strict_kernel<LOPT_SMALL_FC_LOPT>(DevicePlan);
+template __global__ void apply_strict_kernel<LOPT_VELO_MLP>(DevicePlan);
+
+}  // namespace lopt
+
+namespace lopt {
+
+void launch_strict_stats(const DevicePlan &P, cudaStream_t s) {
+  if (P.n_stat_items == 0) return;
+  if (P.kind == LOPT_SMALL_FC_LOPT)
+    stats_strict_kernel<LOPT_SMALL_FC_LOPT><<<P.n_stat_items, kStrictThreads, 0, s>>>(P);
+  else
+    stats_strict_kernel<LOPT_VELO_MLP><<<P.n_stat_items, kStrictThreads, 0, s>>>(P);
+}
+
+void launch_stats_reduce(const DevicePlan &P, cudaStream_t s) {
+  stats_reduce_kernel<<<P.count, 64, 0, s>>>(P);
+}
+
+void launch_strict_apply(const DevicePlan &P, cudaStream_t s) {
+  if (P.n_apply_items == 0) return;
+  if (P.kind == LOPT_SMALL_FC_LOPT)
+    apply_strict_kernel<LOPT_SMALL_FC_LOPT><<<P.n_apply_items, kStrictThreads, 0, s>>>(P);
+  else
+    apply_strict_kernel<LOPT_VELO_MLP><<<P.n_apply_items, kStrictThreads, 0, s>>>(P);
+}
+
+void launch_maxabs_reduce(const DevicePlan &P, cudaStream_t s) {
+  maxabs_reduce_kernel<<<(P.count + 127) / 128, 128, 0, s>>>(P);
+}
+
+}  // namespace lopt

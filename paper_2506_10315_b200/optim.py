@@ -1,0 +1,272 @@
+"""torch.optim front end: the drop-in for the reference's optimizer facade.
+
+Mirrors pkg/src/lopt/optim.py:104-180 (OptimizerHandle + opt_step) behind the
+torch.optim.Optimizer surface PyLO exposes (PAPER.md:586-601:
+`VeLO_CUDA(model.parameters())`, `optimizer.step(loss)`):
+
+  * param_groups with per-group `lr` and `weight_decay` (so
+    torch.optim.lr_scheduler works), or a reference ScheduleConfig sampled at
+    the pre-increment step counter (optim.py:156);
+  * per-step order fixed as in opt_step: accumulators advance, the learned
+    update is scaled by lr, decoupled decay multiplies by f32(1 - lr*wd) last;
+  * state_dict / load_state_dict carry the accumulators {M1,M2,M3,V} (packed
+    per element), the row/column factors and the step counter;
+  * a non-finite gradient raises OptimError naming the tensor and changes
+    nothing (optim.py:160-165, enforced on the device before any write);
+    a non-finite updated parameter raises UpdateOverflowError (engine.py:737)
+    -- unlike the reference, the in-place device update has then already been
+    written (documented in DESIGN.md).
+
+Tensors are stepped through one StepPlan per parameter group; all kernels run
+on the current CUDA stream.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import EngineError, Slot, StepPlan, UpdateOverflowError
+from .features import spec_by_name
+from .schedule import ScheduleConfig, schedule_lr
+from .weights import LoptWeights, random_weights
+
+
+class OptimError(Exception):
+    """optim.py:44-45."""
+
+
+def view_2d(shape) -> tuple:
+    """2-D view of a parameter: rank <= 2 as tensors.py:66-100 (0-D -> (1,1),
+    1-D -> (n,1)); rank > 2 (rejected by the reference, tensors.py:77-78) drops
+    leading 1s while the rank exceeds 2, then flattens to (d0, prod(rest))."""
+    shape = tuple(int(s) for s in shape)
+    while len(shape) > 2 and shape[0] == 1:
+        shape = shape[1:]
+    if len(shape) == 0:
+        return (1, 1)
+    if len(shape) == 1:
+        return (shape[0], 1)
+    if len(shape) == 2:
+        return shape
+    return (shape[0], int(np.prod(shape[1:])))
+
+
+class LearnedOptimizer(torch.optim.Optimizer):
+    """Per-parameter MLP learned optimizer (small_fc_lopt / VeLO-MLP features).
+
+    Args:
+        params: iterable of float32 CUDA parameters or param-group dicts.
+        lr: learning rate scaling the learned update (reference default 1.0).
+        weight_decay: decoupled decay coefficient (optim.py:92-101).
+        feature_set: "small_fc_lopt" (39 features) or "velo_mlp" (29).
+        weights: LoptWeights; default random_weights(d_feat, seed=weights_seed).
+        schedule: optional reference ScheduleConfig; when given it overrides
+            group lr with schedule_lr(schedule, T) at the pre-increment T.
+        mode: "fast" (tensor-core MLP, fp32 tolerance) or "strict" (bitwise).
+        check_errors: synchronize after each step to raise OptimError /
+            UpdateOverflowError like the reference; False keeps steps async
+            (call `check()` to surface errors later).
+    """
+
+    def __init__(self, params, lr: float = 1.0, weight_decay: float = 0.0, *,
+                 feature_set: str = "small_fc_lopt", weights: LoptWeights | None = None,
+                 weights_seed: int = 0, schedule: ScheduleConfig | None = None,
+                 mode: str = "strict", check_errors: bool = True):
+        if lr < 0:
+            raise ValueError(f"invalid learning rate {lr}")
+        if weight_decay < 0:
+            raise ValueError("negative weight decay")
+        if mode not in ("fast", "strict"):
+            raise ValueError(f"unknown mode {mode!r}")
+        super().__init__(params, dict(lr=lr, weight_decay=weight_decay))
+        self.spec = spec_by_name(feature_set)
+        self.lopt_weights = weights or random_weights(self.spec.d_feat, seed=weights_seed)
+        if self.lopt_weights.input_dim != self.spec.d_feat:
+            raise OptimError(f"MLP input dim {self.lopt_weights.input_dim} does not match "
+                             f"feature set ({self.spec.d_feat} columns)")
+        self.schedule = schedule
+        self.mode = mode
+        self.check_errors = check_errors
+        self.T = 0
+        self.last_loss = None
+        self._plans: dict[int, tuple] = {}
+        for group in self.param_groups:
+            for p in group["params"]:
+                if p.dtype != torch.float32:
+                    raise TypeError("the learned-optimizer step is float32 (ParamTensor, "
+                                    "tensors.py:66)")
+
+    # -- state -------------------------------------------------------------
+    def _init_state(self, p):
+        st = self.state[p]
+        if "quad" not in st:
+            m, n = view_2d(p.shape)
+            st["quad"] = torch.zeros(m * n, 4, device=p.device, dtype=torch.float32)
+            st["row_factors"] = torch.zeros(3, m, device=p.device, dtype=torch.float32)
+            st["col_factors"] = torch.zeros(3, n, device=p.device, dtype=torch.float32)
+            st["step"] = self.T
+        return st
+
+    def _slot(self, p, weight_slot=0) -> Slot:
+        st = self._init_state(p)
+        m, n = view_2d(p.shape)
+        if not p.is_contiguous():
+            raise TypeError("parameters must be contiguous")
+        g = p.grad
+        if g.dtype != torch.float32:
+            raise TypeError("gradients must be float32")
+        if not g.is_contiguous():
+            g = p.grad = g.contiguous()
+        return Slot(theta=p.data.view(-1), grad=g.view(-1), state=st["quad"],
+                    r=st["row_factors"], c=st["col_factors"], m=m, n=n, weight_slot=weight_slot)
+
+    def _weights_for_group(self, gi, params):
+        return self.lopt_weights, [0] * len(params)
+
+    def _plan_for_group(self, gi, params):
+        key = tuple(id(p) for p in params)
+        weights, slots_idx = self._weights_for_group(gi, params)
+        slots = [self._slot(p, k) for p, k in zip(params, slots_idx)]
+        cached = self._plans.get(gi)
+        if cached is None or cached[0] != key:
+            plan = StepPlan(slots, self.spec, weights, mode=self.mode)
+            self._plans[gi] = (key, plan, [s.grad.data_ptr() for s in slots])
+        else:
+            _, plan, ptrs = cached
+            now = [s.grad.data_ptr() for s in slots]
+            if now != ptrs:
+                plan.rebind(slots)
+                self._plans[gi] = (key, plan, now)
+        return self._plans[gi][1]
+
+    # -- step --------------------------------------------------------------
+    @torch.no_grad()
+    def step(self, closure=None, loss=None):
+        """optim.py:144-180.  `loss` is accepted (PyLO's step(loss) signature)
+        and recorded; the VeLO subclass feeds it to its hypernetwork."""
+        if closure is not None:
+            with torch.enable_grad():
+                loss = closure()
+        self.last_loss = None if loss is None else float(loss)
+        lr_sched = schedule_lr(self.schedule, self.T) if self.schedule is not None else None
+        launched = []
+        for gi, group in enumerate(self.param_groups):
+            params = [p for p in group["params"] if p.grad is not None]
+            if not params:
+                continue
+            lr = lr_sched if lr_sched is not None else group["lr"]
+            plan = self._plan_for_group(gi, params)
+            self._before_apply(gi, plan, params, loss)
+            self._run_plan(plan, lr, group["weight_decay"], self.T + 1)
+            launched.append((plan, params))
+        self.T += 1
+        for group in self.param_groups:
+            for p in group["params"]:
+                if p in self.state and "quad" in self.state[p]:
+                    self.state[p]["step"] = self.T
+        self._pending = launched
+        if self.check_errors:
+            self.check()
+        return loss
+
+    def _before_apply(self, gi, plan, params, loss):
+        """Hook between plan set-up and the step (VeLO mixes weights here)."""
+
+    # optional list collecting (phase, start_event, end_event) per step; the
+    # benchmark uses it to time the dominant kernel on the launching stream
+    phase_events = None
+
+    def _run_plan(self, plan, lr, weight_decay, t):
+        if self.phase_events is None:
+            plan.step(lr, weight_decay, t)
+            return
+        import torch
+
+        def timed(name, fn):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            self.phase_events.append((name, a, b))
+
+        plan.set_step(lr, weight_decay, t)
+        timed("factors", lambda: (plan.factor_partials(), plan.factor_finalize()))
+        timed("stats", plan.feature_stats)
+        timed("apply", plan.apply)
+
+    def plans(self):
+        """The StepPlans of the parameter groups (one per group)."""
+        return [entry[1] for entry in self._plans.values()]
+
+    def check(self):
+        """Surface device-side errors of the last step (synchronizes)."""
+        for plan, params in getattr(self, "_pending", []):
+            st, _ = plan.status()
+            for j, s in enumerate(st):
+                if s & _lib.LOPT_STATUS_NONFINITE_GRAD:
+                    raise OptimError(f"tensor {self._name(params[j])!r}: non-finite gradient")
+            for j, s in enumerate(st):
+                if s & _lib.LOPT_STATUS_NONFINITE_PARAM:
+                    raise UpdateOverflowError(
+                        f"non-finite parameters after fused step {self._name(params[j])!r}")
+        self._pending = []
+
+    def _name(self, p):
+        for gi, group in enumerate(self.param_groups):
+            for k, q in enumerate(group["params"]):
+                if q is p:
+                    return f"group{gi}.param{k}"
+        return "?"
+
+    def max_abs_updates(self):
+        """UpdateReport.max_abs_update per stepped tensor of the last step."""
+        out = []
+        for plan, _ in getattr(self, "_pending", []) or []:
+            out.extend(plan.status()[1].tolist())
+        return out
+
+    # -- checkpointing -------------------------------------------------------
+    def state_dict(self):
+        sd = super().state_dict()
+        sd["lopt"] = {"T": self.T, "feature_set": self.spec.id.value, "mode": self.mode,
+                      "weights": [(w.copy(), b.copy()) for w, b in self.lopt_weights.layers]}
+        return sd
+
+    def load_state_dict(self, state_dict):
+        extra = state_dict.get("lopt", {})
+        if extra.get("feature_set", self.spec.id.value) != self.spec.id.value:
+            raise OptimError(f"checkpoint feature set {extra['feature_set']!r}, expected "
+                             f"{self.spec.id.value!r}")
+        sd = {k: v for k, v in state_dict.items() if k != "lopt"}
+        super().load_state_dict(sd)
+        for st in self.state.values():
+            for k in ("quad", "row_factors", "col_factors"):
+                if k in st:
+                    st[k] = st[k].to(torch.float32).contiguous()
+        self.T = int(extra.get("T", self.T))
+        self._plans.clear()
+
+
+class AdafacLO_CUDA(LearnedOptimizer):
+    """small_fc_lopt (the Adafactor-featured per-parameter MLP)."""
+
+    def __init__(self, params, lr: float = 1.0, weight_decay: float = 0.0, **kw):
+        kw.setdefault("feature_set", "small_fc_lopt")
+        super().__init__(params, lr=lr, weight_decay=weight_decay, **kw)
+
+
+def opt_step_reference_order(opt: LearnedOptimizer, grads, loss=None):
+    """Functional helper used by tests: assign grads (list in param order)
+    and step, like opt_step(h, grads, loss) (optim.py:144)."""
+    ps = [p for g in opt.param_groups for p in g["params"]]
+    if len(grads) != len(ps):
+        raise OptimError(f"got {len(grads)} gradients for {len(ps)} tensors")
+    for p, g in zip(ps, grads):
+        if tuple(g.shape) != tuple(p.shape):
+            raise OptimError(f"gradient {tuple(g.shape)} vs param {tuple(p.shape)}")
+        p.grad = g
+    return opt.step(loss=loss)
