@@ -32,7 +32,7 @@ EXPORTS = [
     "lopt_factor_partials", "lopt_factor_finalize", "lopt_feature_stats", "lopt_apply",
     "lopt_step", "lopt_factor_sums_ptr", "lopt_stat_sums_ptr", "lopt_status_ptr",
     "lopt_read_status", "lopt_debug_ptrs", "lopt_version",
-    "lopt_num_kernels_launched_last_step", "lopt_velo_mix",
+    "lopt_num_kernels_launched_last_step", "lopt_velo_mix", "lopt_selftest_umma",
 ]
 
 
@@ -121,6 +121,7 @@ def lib(required: bool = True):
     L.lopt_version.restype = ctypes.c_char_p
     L.lopt_num_kernels_launched_last_step.argtypes = [vp]
     L.lopt_velo_mix.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp]
+    L.lopt_selftest_umma.argtypes = [i32, i32, vp, vp, vp, vp]
     for name in EXPORTS:
         f = getattr(L, name)
         if name != "lopt_version":

@@ -27,6 +27,7 @@ void launch_fast_stats(const DevicePlan &P, cudaStream_t s);
 void launch_fast_apply(const DevicePlan &P, cudaStream_t s);
 int64_t fast_stat_chunk();
 int64_t fast_apply_chunk();
+size_t prep_image_bytes();
 }  // namespace lopt
 
 using namespace lopt;
@@ -53,9 +54,11 @@ struct lopt_plan {
   std::vector<ChunkItem> sitems, aitems;
   int64_t max_mn = 0;        // max over tensors of m + n
   int64_t factor_sums = 0;   // f64 entries of the all-reducible factor block
+  int64_t n_tiles = 0;       // fast path: 128-element tiles
   // workspace regions
   Region r_desc, r_fitems, r_sitems, r_aitems, r_tscal, r_step, r_status, r_maxabs, r_imaxabs,
-      r_abort, r_fsums, r_rowpart, r_colpart, r_rowtab, r_coltab, r_statpart, r_sumsq, r_weights;
+      r_abort, r_fsums, r_rowpart, r_colpart, r_rowtab, r_coltab, r_statpart, r_sumsq, r_weights,
+      r_prep, r_bcsum;
   size_t ws_bytes = 0;
   char *ws = nullptr;
   DevicePlan dp{};
@@ -163,8 +166,14 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
       p->sitems.push_back(ChunkItem{j, 0, e, std::min<int64_t>(t.hi, e + stat_chunk)});
     d.stat_items = (int32_t)p->sitems.size() - d.stat_item0;
     d.apply_item0 = (int32_t)p->aitems.size();
-    for (int64_t e = t.lo; e < t.hi; e += apply_chunk)
-      p->aitems.push_back(ChunkItem{j, 0, e, std::min<int64_t>(t.hi, e + apply_chunk)});
+    d.tile0 = p->n_tiles;
+    if (fast) {
+      // the persistent tensor-core kernel walks 128-element tiles implicitly
+      p->n_tiles += (t.hi - t.lo + apply_chunk - 1) / apply_chunk;
+    } else {
+      for (int64_t e = t.lo; e < t.hi; e += apply_chunk)
+        p->aitems.push_back(ChunkItem{j, 0, e, std::min<int64_t>(t.hi, e + apply_chunk)});
+    }
     d.apply_items = (int32_t)p->aitems.size() - d.apply_item0;
   }
   p->factor_sums = rows + cols;
@@ -195,6 +204,8 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   take(p->r_statpart, sizeof(double) * D * std::max<size_t>(1, p->sitems.size()));
   take(p->r_sumsq, sizeof(double) * D * count);
   take(p->r_weights, sizeof(float) * (size_t)wstride * cfg->num_weight_sets);
+  take(p->r_prep, fast ? prep_image_bytes() * count : 16);
+  take(p->r_bcsum, fast ? sizeof(double) * D * count : 16);
   p->ws_bytes = align_up(off, 256);
   // device plan (pointers filled at bind time)
   DevicePlan &P = p->dp;
@@ -211,6 +222,7 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   for (int k = 0; k < 7; k++) P.beta[k] = (float)cfg->betas[k];
   P.alpha = cfg->alpha;
   P.beta_out = cfg->beta_out;
+  P.n_tiles = p->n_tiles;
   if (fast && !fast_supported(P)) {
     delete p;
     return LOPT_ERR_UNSUPPORTED;
@@ -275,7 +287,11 @@ int lopt_bind_workspace(lopt_plan *p, void *dev_ptr, size_t bytes, void *stream)
   P.maxabs = (float *)(ws + p->r_maxabs.off);
   P.item_maxabs = (float *)(ws + p->r_imaxabs.off);
   P.abort_flag = (uint32_t *)(ws + p->r_abort.off);
+  const bool fast = p->cfg.mode == LOPT_MODE_FAST;
+  P.prep = fast ? (unsigned char *)(ws + p->r_prep.off) : nullptr;
+  P.bcsum = fast ? (double *)(ws + p->r_bcsum.off) : nullptr;
   int st;
+  if ((st = check_cuda(cudaMemsetAsync(ws + p->r_bcsum.off, 0, p->r_bcsum.bytes, s)))) return st;
   // descriptor uploads: pageable source, so the copies complete before return
   if ((st = check_cuda(cudaMemcpyAsync(P.tensors, p->descs.data(),
                                        sizeof(TensorDesc) * p->descs.size(),
@@ -366,6 +382,8 @@ int lopt_factor_partials(lopt_plan *p, void *stream) {
     return st;
   if ((st = check_cuda(cudaMemsetAsync(p->ws + p->r_abort.off, 0, p->r_abort.bytes, s))))
     return st;
+  if ((st = check_cuda(cudaMemsetAsync(p->ws + p->r_maxabs.off, 0, p->r_maxabs.bytes, s))))
+    return st;
   p->launches_last_step = 0;
   if (p->cfg.state_advanced) return LOPT_OK;
   launch_factor_partials(p->dp, s);
@@ -386,11 +404,12 @@ int lopt_factor_finalize(lopt_plan *p, void *stream) {
 int lopt_feature_stats(lopt_plan *p, void *stream) {
   if (!p || !p->ws) return LOPT_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  if (p->cfg.mode == LOPT_MODE_FAST)
+  if (p->cfg.mode == LOPT_MODE_FAST) {
     launch_fast_stats(p->dp, s);
-  else
+  } else {
     launch_strict_stats(p->dp, s);
-  launch_stats_reduce(p->dp, s);
+    launch_stats_reduce(p->dp, s);
+  }
   p->launches_last_step += (p->dp.n_stat_items > 0) + 1;
   return check_launch();
 }
@@ -398,12 +417,14 @@ int lopt_feature_stats(lopt_plan *p, void *stream) {
 int lopt_apply(lopt_plan *p, void *stream) {
   if (!p || !p->ws) return LOPT_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  if (p->cfg.mode == LOPT_MODE_FAST)
-    launch_fast_apply(p->dp, s);
-  else
+  if (p->cfg.mode == LOPT_MODE_FAST) {
+    launch_fast_apply(p->dp, s);   // prep + persistent tensor-core apply
+    p->launches_last_step += 1 + (p->dp.n_tiles > 0);
+  } else {
     launch_strict_apply(p->dp, s);
-  launch_maxabs_reduce(p->dp, s);
-  p->launches_last_step += (p->dp.n_apply_items > 0) + 1;
+    launch_maxabs_reduce(p->dp, s);
+    p->launches_last_step += (p->dp.n_apply_items > 0) + 1;
+  }
   return check_launch();
 }
 

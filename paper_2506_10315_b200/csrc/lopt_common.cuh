@@ -17,7 +17,10 @@ constexpr int kMaxHidden = 32;        // compiled MLP width (reference optimizer
 constexpr float kEpsRecip = 1e-12f;   // features.py:66
 constexpr double kEpsNorm = 1e-5;     // features.py:67
 constexpr float kClip = 0.1f;         // features.py:82
-constexpr int kRowTab = 8;            // row/col table stride: x5,x6,x7, rsqrt(x+eps) x3, pad
+// row/col table entry (16 x 32-bit): f32 {x5, x6, x7, rsqrt(x5+eps) | rsqrt(x6+eps),
+// rsqrt(x7+eps), 0, 0} then, for the fast path, the six values split into bf16
+// hi/lo pairs {hi01, hi23, hi45, 0 | lo01, lo23, lo45, 0}
+constexpr int kRowTab = 16;
 
 __host__ __device__ constexpr int d_feat(int kind) { return kind == LOPT_SMALL_FC_LOPT ? 39 : 29; }
 
@@ -42,6 +45,7 @@ struct TensorDesc {
   int32_t stat_item0, stat_items;   // phase-1 items of this tensor (contiguous)
   int32_t apply_item0, apply_items; // phase-2 items of this tensor (contiguous)
   int32_t pad_;
+  int64_t tile0;          // fast path: first 128-element tile of this tensor
 };
 
 // Phase-0 tile: rows [a0, a1) x columns [b0, b1) of one tensor.
@@ -92,6 +96,10 @@ struct DevicePlan {
   int32_t weight_stride, state_advanced;
   float beta[7];          // f32(beta) as the reference casts them (state.py:81)
   float alpha, beta_out;
+  // fast path
+  int64_t n_tiles;        // 128-element tiles over all tensors
+  unsigned char *prep;    // per-tensor PrepImage (B operands, layer-3 weights)
+  double *bcsum;          // [count x d_feat] closed-form sums of broadcast features
 };
 
 __host__ __device__ inline int weight_stride(int d, int h1, int h2) {

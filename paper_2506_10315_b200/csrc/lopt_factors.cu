@@ -8,6 +8,7 @@
 // multi-GPU caller all-reduces (distsim.py:448-474).  No float atomics: the
 // result is bit-reproducible for a fixed plan.
 #include "lopt_common.cuh"
+#include "lopt_tc.cuh"
 
 namespace lopt {
 
@@ -152,35 +153,79 @@ __global__ void factor_finalize_kernel(DevicePlan P) {
       fac[k * len + i] = x[k];
     }
   }
-  float4 lo4 = make_float4(x[0], x[1], x[2], rsqrt_strict(x[0]));
-  float4 hi4 = make_float4(rsqrt_strict(x[1]), rsqrt_strict(x[2]), 0.f, 0.f);
-  reinterpret_cast<float4 *>(tab)[0] = lo4;
-  reinterpret_cast<float4 *>(tab)[1] = hi4;
+  const float v6[6] = {x[0], x[1], x[2], rsqrt_strict(x[0]), rsqrt_strict(x[1]),
+                       rsqrt_strict(x[2])};
+  uint32_t hi[3], lo[3];
+#pragma unroll
+  for (int q = 0; q < 3; q++) tc::split_pair(v6[2 * q], v6[2 * q + 1], hi[q], lo[q]);
+  float4 *t4 = reinterpret_cast<float4 *>(tab);
+  t4[0] = make_float4(v6[0], v6[1], v6[2], v6[3]);
+  t4[1] = make_float4(v6[4], v6[5], 0.f, 0.f);
+  reinterpret_cast<uint4 *>(tab)[2] = make_uint4(hi[0], hi[1], hi[2], 0u);
+  reinterpret_cast<uint4 *>(tab)[3] = make_uint4(lo[0], lo[1], lo[2], 0u);
 }
 
 // features.py:133-135: mr_i = f32(mean_f64(r_i')).  One CTA per tensor,
 // fixed-order f64 reduction.
+// Fast mode also produces the closed-form feature sums of the 12 row/column
+// broadcast columns over this call's elements [lo, hi): sum_a cnt_a * x(a)^2
+// and sum_b cnt_b * y(b)^2, so phase 1 only has to reduce the per-element
+// columns.
 __global__ void __launch_bounds__(256) factor_means_kernel(DevicePlan P) {
   const TensorDesc T = P.tensors[blockIdx.x];
-  __shared__ double red[3][8];
-  double acc[3] = {0.0, 0.0, 0.0};
+  constexpr int NW = 256 / 32;
+  __shared__ double red[15][NW];
+  const bool bc = P.bcsum != nullptr;
+  double acc[15];
+#pragma unroll
+  for (int k = 0; k < 15; k++) acc[k] = 0.0;
   for (int64_t a = threadIdx.x; a < T.m; a += blockDim.x) {
     const float4 v = reinterpret_cast<const float4 *>(T.rowtab + a * kRowTab)[0];
     acc[0] += (double)v.x;
     acc[1] += (double)v.y;
     acc[2] += (double)v.z;
+    if (bc) {
+      const float4 w = reinterpret_cast<const float4 *>(T.rowtab + a * kRowTab)[1];
+      const int64_t s0 = max(T.lo, a * T.n), s1 = min(T.hi, (a + 1) * T.n);
+      const double cnt = s1 > s0 ? (double)(s1 - s0) : 0.0;
+      const float x6[6] = {v.x, v.y, v.z, v.w, w.x, w.y};
+#pragma unroll
+      for (int k = 0; k < 6; k++) acc[3 + k] += cnt * (double)x6[k] * (double)x6[k];
+    }
+  }
+  if (bc) {
+    for (int64_t b = threadIdx.x; b < T.n; b += blockDim.x) {
+      // rows a with lo <= a*n + b < hi
+      const int64_t alo = T.lo > b ? (T.lo - b + T.n - 1) / T.n : 0;
+      const int64_t ahi = T.hi - 1 >= b ? (T.hi - 1 - b) / T.n : -1;
+      const double cnt = ahi >= alo ? (double)(ahi - alo + 1) : 0.0;
+      const float4 v = reinterpret_cast<const float4 *>(T.coltab + b * kRowTab)[0];
+      const float4 w = reinterpret_cast<const float4 *>(T.coltab + b * kRowTab)[1];
+      const float y6[6] = {v.x, v.y, v.z, v.w, w.x, w.y};
+#pragma unroll
+      for (int k = 0; k < 6; k++) acc[9 + k] += cnt * (double)y6[k] * (double)y6[k];
+    }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < 3; k++) {
+  for (int k = 0; k < 15; k++) {
     const double s = warp_sum(acc[k]);
     if (lane == 0) red[k][warp] = s;
   }
   __syncthreads();
-  if (threadIdx.x < 3) {
+  if (threadIdx.x < 15) {
     double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += red[threadIdx.x][w];
-    P.tscal[blockIdx.x].mr[threadIdx.x] = (float)(s / (double)T.m);
+    for (int w = 0; w < NW; w++) s += red[threadIdx.x][w];
+    const int k = threadIdx.x;
+    if (k < 3) {
+      P.tscal[blockIdx.x].mr[k] = (float)(s / (double)T.m);
+    } else if (bc) {
+      // reference columns: r5,r6,r7 -> 4,5,6; rsqrt r -> 14,15,16;
+      // c5,c6,c7 -> 7,8,9; rsqrt c -> 17,18,19
+      const int q = k - 3;
+      const int col = q < 6 ? (q < 3 ? 4 + q : 11 + q) : (q < 9 ? 1 + q : 8 + q);
+      P.bcsum[(int64_t)blockIdx.x * d_feat(P.kind) + col] = s;
+    }
   }
 }
 
