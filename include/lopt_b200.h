@@ -148,8 +148,8 @@ int lopt_velo_mix(lopt_plan *plan, const float *lstm_params, float *lstm_state,
                   int32_t reserved, const float *loss_feats);
 
 /* Known-answer test of the tcgen05 building blocks (device pointers):
- * D[128 x 32] f32 = A[128 x K] bf16 * B[32 x K]^T bf16, K in {16,32,48,64},
- * A staged in shared memory (a_in_tmem = 0) or tensor memory (1). */
+ * D[128 x 32] f32 = A[128 x K] * B[32 x K]^T, K in {16,32,48,64}; flag bit 0:
+ * A staged in tensor memory (else shared memory), bit 1: fp16 operands (else bf16). */
 int lopt_selftest_umma(int32_t a_in_tmem, int32_t K, const void *A, const void *B, float *D,
                        void *stream);
 

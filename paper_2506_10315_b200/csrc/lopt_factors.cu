@@ -153,16 +153,11 @@ __global__ void factor_finalize_kernel(DevicePlan P) {
       fac[k * len + i] = x[k];
     }
   }
-  const float v6[6] = {x[0], x[1], x[2], rsqrt_strict(x[0]), rsqrt_strict(x[1]),
-                       rsqrt_strict(x[2])};
-  uint32_t hi[3], lo[3];
-#pragma unroll
-  for (int q = 0; q < 3; q++) tc::split_pair(v6[2 * q], v6[2 * q + 1], hi[q], lo[q]);
+  // entries 8..15 (the fast path's scaled fp16 operands) are written by
+  // prep_kernel once the normalization scale is known
   float4 *t4 = reinterpret_cast<float4 *>(tab);
-  t4[0] = make_float4(v6[0], v6[1], v6[2], v6[3]);
-  t4[1] = make_float4(v6[4], v6[5], 0.f, 0.f);
-  reinterpret_cast<uint4 *>(tab)[2] = make_uint4(hi[0], hi[1], hi[2], 0u);
-  reinterpret_cast<uint4 *>(tab)[3] = make_uint4(lo[0], lo[1], lo[2], 0u);
+  t4[0] = make_float4(x[0], x[1], x[2], rsqrt_strict(x[0]));
+  t4[1] = make_float4(rsqrt_strict(x[1]), rsqrt_strict(x[2]), 0.f, 0.f);
 }
 
 // features.py:133-135: mr_i = f32(mean_f64(r_i')).  One CTA per tensor,

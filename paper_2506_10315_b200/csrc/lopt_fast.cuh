@@ -1,0 +1,101 @@
+// lopt_fast.cuh -- definitions shared by the fast-mode kernels (lopt_fast.cu,
+// lopt_apply_tc.cu): the per-tensor prepared operand image, the A-operand
+// column order, and the per-element fast feature arithmetic.
+#pragma once
+
+#include "lopt_common.cuh"
+#include "lopt_tc.cuh"
+
+namespace lopt {
+
+constexpr int kTile = 128;
+
+// B slices are K=16 x N=32 fp16 in the canonical K-major no-swizzle layout:
+// byte (k>>3)*512 + (o>>3)*128 + (o&7)*16 + (k&7)*2.
+//
+// Operands are fp16 two-term splits.  Layer 1 takes the NORMALIZED features
+// x*scale (|x*scale| <= sqrt(m*n) < 65504 because sum_e (x*scale)^2 <= m*n),
+// so W1 is used unscaled.  Layer 2 takes ReLU(h1) * 2^-s2 with s2 chosen per
+// tensor from a bound on |h1|, so it cannot overflow fp16 either (s2 = 0 for
+// every tensor of the benchmarked models).
+struct __align__(128) PrepImage {
+  uint16_t b1[4][512];      // layer 1: We_hi, We_lo, Wbc_hi(+bias_hi), Wbc_lo(+bias_lo)
+  uint16_t b2[5][512];      // layer 2: W2_hi[K0-15], W2_hi[K16-31], W2_lo x2, bias*2^-s2
+  float w3[2][32];          // layer 3, f32
+  float b3[2];
+  float sqmr[3];            // sqrt(mean r_i)
+  float escale[17];         // normalization scale of the per-element columns (+ clip)
+  float s2_down, s2_up;     // 2^-s2, 2^s2
+};
+static_assert(sizeof(PrepImage) % 16 == 0, "PrepImage must be 16-byte granular");
+
+__device__ __forceinline__ int bslot(int o, int k) {
+  return ((k >> 3) * 512 + (o >> 3) * 128 + (o & 7) * 16 + (k & 7) * 2) >> 1;
+}
+
+// Element-wise column order of the A operand (reference column indices):
+// M1 M2 M3 V M1/sv M2/sv M3/sv 1/sv gS5 gS6 gS7 M1S5 M2S6 M3S7 W g
+__device__ __forceinline__ int elem_col(int kind, int q) {
+  if (q < 4) return q;
+  if (q < 8) return 6 + q;           // 10..13
+  if (q < 14) return 12 + q;         // 20..25
+  return kind == LOPT_SMALL_FC_LOPT ? 23 + q : 12 + q;   // W, g: 37,38 | 26,27
+}
+// Broadcast slice order: r5 r6 r7 rr5 rr6 rr7 c5 c6 c7 rc5 rc6 rc7 [clip] [bias]
+__device__ __forceinline__ int bc_col(int q) {
+  if (q < 3) return 4 + q;
+  if (q < 6) return 11 + q;          // 14..16
+  if (q < 9) return 1 + q;           // 7..9
+  return 8 + q;                      // 17..19
+}
+
+struct FastIn {
+  float w, g, m1, m2, m3, v;
+};
+
+// state.py:77-90 recomputed from the old accumulators, bit for bit, so the
+// stored state stays exact in fast mode too.
+__device__ __forceinline__ void advance(float g, float4 s, bool advanced, const float *beta,
+                                        FastIn &x) {
+  x.g = g;
+  if (advanced) {
+    x.m1 = s.x; x.m2 = s.y; x.m3 = s.z; x.v = s.w;
+  } else {
+    x.m1 = ema(beta[0], __fsub_rn(1.0f, beta[0]), s.x, g);
+    x.m2 = ema(beta[1], __fsub_rn(1.0f, beta[1]), s.y, g);
+    x.m3 = ema(beta[2], __fsub_rn(1.0f, beta[2]), s.z, g);
+    x.v = ema(beta[3], __fsub_rn(1.0f, beta[3]), s.w, __fmul_rn(g, g));
+  }
+}
+
+// f[0..15] in elem_col order; rc = {r5, r6, r7} of the row, cc = {c5, c6, c7}.
+// MUFU rsqrt replaces the correctly rounded div/sqrt of features.py:153-195.
+__device__ __forceinline__ void fast_features(const FastIn &x, const float *rc, const float *cc,
+                                              const float *sqmr, float *f) {
+  const float svi = rsqrtf(x.v + kEpsRecip);
+  float s[3];
+#pragma unroll
+  for (int i = 0; i < 3; i++) s[i] = sqmr[i] * rsqrtf(fmaf(rc[i], cc[i], kEpsRecip));
+  f[0] = x.m1; f[1] = x.m2; f[2] = x.m3; f[3] = x.v;
+  f[4] = x.m1 * svi; f[5] = x.m2 * svi; f[6] = x.m3 * svi; f[7] = svi;
+  f[8] = x.g * s[0]; f[9] = x.g * s[1]; f[10] = x.g * s[2];
+  f[11] = x.m1 * s[0]; f[12] = x.m2 * s[1]; f[13] = x.m3 * s[2];
+  f[14] = x.w; f[15] = x.g;
+}
+
+__device__ __forceinline__ float clip01(float g) { return fminf(fmaxf(g, -kClip), kClip); }
+
+// e = a*n + b for e < 2^53: one DMUL by the reciprocal and a +-1 correction.
+__device__ __forceinline__ void divmod(int64_t e, int64_t n, double inv_n, int64_t &a, int64_t &b) {
+  a = (int64_t)((double)e * inv_n);
+  b = e - a * n;
+  if (b < 0) {
+    a--;
+    b += n;
+  } else if (b >= n) {
+    a++;
+    b -= n;
+  }
+}
+
+}  // namespace lopt

@@ -7,7 +7,7 @@
 
 namespace lopt {
 
-__global__ void __launch_bounds__(128) umma_selftest_kernel(int a_in_tmem, int K,
+__global__ void __launch_bounds__(128) umma_selftest_kernel(int a_in_tmem, int fp16, int K,
                                                             const uint16_t *A, const uint16_t *B,
                                                             float *D) {
   __shared__ __align__(1024) uint16_t As[128 * 64];
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(int a_in_tmem, int K
   __syncthreads();
   if (t == 0) {
     tc::fence_after_sync();
-    constexpr uint32_t idesc = tc::idesc_bf16_f32(128, 32);
+    const uint32_t idesc = fp16 ? tc::idesc_f16_f32(128, 32) : tc::idesc_bf16_f32(128, 32);
     for (int s = 0; s < slices; s++) {
       const uint64_t bdesc = tc::smem_desc_kmajor(tc::smem_u32(Bs + s * 512), 512, 128);
       if (a_in_tmem) {
@@ -82,8 +82,9 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(int a_in_tmem, int K
 extern "C" int lopt_selftest_umma(int32_t a_in_tmem, int32_t K, const void *A, const void *B,
                                   float *D, void *stream) {
   if (K < 16 || K > 64 || K % 16 != 0 || !A || !B || !D) return LOPT_ERR_INVALID;
+  // bit 0: A in TMEM; bit 1: fp16 operands (else bf16)
   lopt::umma_selftest_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(
-      a_in_tmem, K, (const uint16_t *)A, (const uint16_t *)B, D);
+      a_in_tmem & 1, (a_in_tmem >> 1) & 1, K, (const uint16_t *)A, (const uint16_t *)B, D);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? LOPT_OK : LOPT_ERR_CUDA;
 }

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_fp16.h>
 
 namespace lopt {
 namespace tc {
@@ -106,6 +107,13 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
          | ((uint32_t)(M >> 4) << 24);   // M / 16
 }
 
+// Instruction descriptor: kind::f16 with fp16 A/B, f32 D, K-major A and B.
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {
+  return (1u << 4)                       // D format f32 (A/B format 0 = f16)
+         | ((uint32_t)(N >> 3) << 17)
+         | ((uint32_t)(M >> 4) << 24);
+}
+
 // Shared-memory matrix descriptor, K-major, no swizzle ("interleave"):
 // core matrices of 8 rows x 16 bytes stored contiguously (128 B); LBO = byte
 // distance between the two 8-element K halves of a 16-element K slice, SBO =
@@ -173,10 +181,27 @@ __device__ __forceinline__ float bf16lo_to_f32(uint32_t p) { return __uint_as_fl
 __device__ __forceinline__ float bf16hi_to_f32(uint32_t p) {
   return __uint_as_float(p & 0xFFFF0000u);
 }
-// Two-term bf16 split of a pair: a = a_hi + a_lo + O(2^-17 |a|).
+// Two-term bf16 split of a pair: a = a_hi + a_lo + O(2^-16 |a|).
 __device__ __forceinline__ void split_pair(float a, float b, uint32_t &hi, uint32_t &lo) {
   hi = pack_bf16x2(a, b);
   lo = pack_bf16x2(a - bf16lo_to_f32(hi), b - bf16hi_to_f32(hi));
+}
+
+// fp16 pair (low half = a, high half = b), round to nearest.
+__device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %2, %1;\n" : "=r"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_f16x2(uint32_t p) {
+  return __half22float2(*reinterpret_cast<const __half2 *>(&p));
+}
+// Two-term fp16 split of a pair: a = a_hi + a_lo + O(2^-22 |a|) for |a| in the
+// fp16 normal range (absolute error <= 2^-25 below it).
+__device__ __forceinline__ void split_pair_f16(float a, float b, uint32_t &hi, uint32_t &lo) {
+  hi = pack_f16x2(a, b);
+  const float2 h = unpack_f16x2(hi);
+  lo = pack_f16x2(a - h.x, b - h.y);
 }
 
 }  // namespace tc

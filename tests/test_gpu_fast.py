@@ -84,7 +84,7 @@ def test_fast_optimizer_steps_vs_oracle(P, oracle, feature_set, which):
 
     shapes = SHAPE_SETS[which]
     rng = np.random.default_rng(5)
-    init = [(rng.standard_normal(s) * 0.02).astype(F32) for s in shapes]
+    init = [np.asarray(rng.standard_normal(s) * 0.02, dtype=F32) for s in shapes]
     params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
     opt = P.LearnedOptimizer(params, feature_set=feature_set, mode="fast", weight_decay=0.01)
     o_params = [x.reshape(P.view_2d(x.shape)).copy() for x in init]
@@ -103,6 +103,7 @@ def test_fast_optimizer_steps_vs_oracle(P, oracle, feature_set, which):
         oracle.opt_step(o_params, o_states, grads, w, kind, 1.0, weight_decay=0.01, threads=8)
         for p, q in zip(params, o_params):
             worst = max(worst, _close(p.detach().cpu().numpy(), q))
+    print(f"max elementwise err/(1+|theta|) {which} {feature_set}: {worst:.3e}")
     assert worst <= TOL, worst
     for p, s in zip(params, o_states):
         quad = opt.state[p]["quad"].cpu().numpy()
@@ -139,7 +140,8 @@ def test_fast_hundred_steps_relative_l2(P, oracle, feature_set):
         got = p.detach().cpu().numpy().reshape(-1).astype(np.float64)
         want = q.reshape(-1).astype(np.float64)
         rel = np.linalg.norm(got - want) / np.linalg.norm(want)
-        assert rel <= 1e-5, rel
+        print(f"100-step relL2 {feature_set} {p.shape}: {rel:.3e}")
+        assert rel <= 2e-6, rel
     for p, s in zip(params, o_states):
         quad = opt.state[p]["quad"].cpu().numpy()
         assert quad[:, 0].tobytes() == s.M[0].reshape(-1).tobytes()
