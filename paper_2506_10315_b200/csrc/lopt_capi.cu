@@ -126,6 +126,9 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
         d.nstrips = 1;
         d.nrowblocks = (int32_t)((t.m + kFactorTileElems - 1) / kFactorTileElems);
         for (int rb = 0; rb < d.nrowblocks; rb++) {
+          // row blocks outside this call's element range keep zero partials
+          const int64_t r0 = rb * kFactorTileElems, r1 = std::min<int64_t>(t.m, r0 + kFactorTileElems);
+          if (r1 <= t.lo || r0 >= t.hi) continue;
           FactorItem it{};
           it.tensor = j;
           it.strip = 0;
@@ -145,6 +148,8 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
         d.nrowblocks = (int32_t)((t.m + R - 1) / R);
         for (int rb = 0; rb < d.nrowblocks; rb++)
           for (int s = 0; s < d.nstrips; s++) {
+            const int64_t e0 = rb * R * t.n, e1 = std::min<int64_t>(t.m, (rb + 1) * R) * t.n;
+            if (e1 <= t.lo || e0 >= t.hi) continue;
             FactorItem it{};
             it.tensor = j;
             it.strip = s;
@@ -176,7 +181,7 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
     }
     d.apply_items = (int32_t)p->aitems.size() - d.apply_item0;
   }
-  p->factor_sums = rows + cols;
+  p->factor_sums = rows + cols + 1;   // + the non-finite-gradient flag slot
   // workspace layout
   size_t off = 0;
   auto take = [&](Region &r, size_t bytes) {
@@ -287,6 +292,7 @@ int lopt_bind_workspace(lopt_plan *p, void *dev_ptr, size_t bytes, void *stream)
   P.maxabs = (float *)(ws + p->r_maxabs.off);
   P.item_maxabs = (float *)(ws + p->r_imaxabs.off);
   P.abort_flag = (uint32_t *)(ws + p->r_abort.off);
+  P.grad_flag = fsums + (p->factor_sums - 1);
   const bool fast = p->cfg.mode == LOPT_MODE_FAST;
   P.prep = fast ? (unsigned char *)(ws + p->r_prep.off) : nullptr;
   P.bcsum = fast ? (double *)(ws + p->r_bcsum.off) : nullptr;
@@ -384,6 +390,7 @@ int lopt_factor_partials(lopt_plan *p, void *stream) {
     return st;
   if ((st = check_cuda(cudaMemsetAsync(p->ws + p->r_maxabs.off, 0, p->r_maxabs.bytes, s))))
     return st;
+  if ((st = check_cuda(cudaMemsetAsync(p->dp.grad_flag, 0, sizeof(double), s)))) return st;
   p->launches_last_step = 0;
   if (p->cfg.state_advanced) return LOPT_OK;
   launch_factor_partials(p->dp, s);

@@ -91,6 +91,8 @@ struct DevicePlan {
   float *maxabs;          // [count]
   float *item_maxabs;     // [n_apply_items]
   uint32_t *abort_flag;   // any non-finite gradient in this step
+  double *grad_flag;      // last slot of the factor-sum block: > 0 if any rank saw a
+                          // non-finite gradient (all-reduced with the sums)
   int32_t count, n_factor_items, n_stat_items, n_apply_items;
   int32_t kind, mode, h1, h2;
   int32_t weight_stride, state_advanced;

@@ -56,6 +56,7 @@ factor_partials_kernel(DevicePlan P) {
       if (bad_s) {
         atomicOr(&P.status[it.tensor], LOPT_STATUS_NONFINITE_GRAD);
         atomicOr(P.abort_flag, 1u);
+        *P.grad_flag = 1.0;
       }
     }
     return;
@@ -106,6 +107,7 @@ factor_partials_kernel(DevicePlan P) {
   if (tid == 0 && bad_s) {
     atomicOr(&P.status[it.tensor], LOPT_STATUS_NONFINITE_GRAD);
     atomicOr(P.abort_flag, 1u);
+    *P.grad_flag = 1.0;
   }
 }
 
@@ -144,6 +146,13 @@ __global__ void factor_finalize_kernel(DevicePlan P) {
     for (int k = 0; k < 3; k++) x[k] = fac[k * len + i];
   } else {
     const double sum = is_row ? T.rowsum[i] : T.colsum[i];
+    if (*P.grad_flag != 0.0) {
+      // a non-finite gradient on any rank (the flag is all-reduced with the
+      // sums): abort before any state is written (optim.py:160-165)
+      if (!isfinite(sum)) atomicOr(&P.status[blockIdx.y], LOPT_STATUS_NONFINITE_GRAD);
+      atomicOr(P.abort_flag, 1u);
+      return;
+    }
     const float mean = (float)(sum / (double)(is_row ? T.n : T.m));
 #pragma unroll
     for (int k = 0; k < 3; k++) {

@@ -1,0 +1,155 @@
+"""Data-parallel sharded optimizer step over torch.distributed (NCCL on GPUs).
+
+The reference simulates three strategies in distsim.py; this module runs the
+element-range one for real (REDUCE_SCATTER, distsim.py:403-534) and keeps the
+whole-tensor ownership plan of FSDP_A2A (distsim.py:99-123) available as a
+partition helper:
+
+  * parameters are flattened into one arena (like ZeRO / FSDP flat params) and
+    rank r owns the contiguous slice [r*S, (r+1)*S) of it; for every tensor
+    this yields an element range [lo, hi) (possibly empty), so optimizer state
+    is held for 1/N of the elements only;
+  * phase 0 computes f64 partial row/column sums of g^2 over the local
+    elements; one all-reduce (sum, float64) of the contiguous factor block
+    merges them -- the "factor merge" of distsim.py:427-476;
+  * phase 1 computes f64 feature sums over the local elements; one all-reduce
+    of the [tensors x d_feat] block merges them -- the "stats merge",
+    normalization_across_shards (distsim.py:598-610);
+  * phase 2 updates the local slice in place; one all-gather of the flat
+    parameter arena (in place, NCCL over NVLink) replaces the "parameter
+    gather" (distsim.py:523-530).
+
+Merging f64 partials reproduces the single-device f32 factors and scales
+(SURVEY.md Appendix A), so the sharded step matches the 1-GPU step.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .engine import Slot, StepPlan
+from .optim import LearnedOptimizer, view_2d
+
+
+def worker_ranges(lo: int, hi: int, workers: int):
+    """engine.py:597-605: split [lo, hi) into `workers` ranges, sizes within 1."""
+    if workers < 1:
+        raise ValueError("worker count must be >= 1")
+    span = hi - lo
+    b = [lo + span * w // workers for w in range(workers + 1)]
+    return [(b[w], b[w + 1]) for w in range(workers)]
+
+
+def flat_shard_ranges(sizes, world: int, rank: int):
+    """Per-tensor local ranges of rank `rank` when the concatenation of the
+    tensors (in order) is cut into `world` equal contiguous slices (the arena
+    is padded to a multiple of `world`).  Returns (ranges, slice_len, padded)."""
+    total = int(sum(sizes))
+    padded = (total + world - 1) // world * world
+    S = padded // world
+    s0, s1 = rank * S, (rank + 1) * S
+    out, off = [], 0
+    for n in sizes:
+        lo, hi = max(off, s0) - off, min(off + n, s1) - off
+        out.append((lo, hi) if hi > lo else (0, 0))
+        off += n
+    return out, S, padded
+
+
+def owner_plan(sizes, workers: int):
+    """distsim.py:109-118 FSDP_A2A ownership: greedy largest-first."""
+    order = sorted(range(len(sizes)), key=lambda j: -sizes[j])
+    load = [0] * workers
+    owner = [0] * len(sizes)
+    for j in order:
+        w = min(range(workers), key=lambda i: (load[i], i))
+        owner[j] = w
+        load[w] += sizes[j]
+    return owner
+
+
+class ShardedLearnedOptimizer(LearnedOptimizer):
+    """LearnedOptimizer whose step is sharded by element ranges across the
+    ranks of the default process group.  Parameters must be identical on all
+    ranks at construction; gradients are expected to be already reduced
+    (e.g. DDP), of which each rank reads only its own slice."""
+
+    def __init__(self, params, *args, process_group=None, **kw):
+        super().__init__(params, *args, **kw)
+        self.pg = process_group
+        self.world = dist.get_world_size(self.pg)
+        self.rank = dist.get_rank(self.pg)
+        if len(self.param_groups) != 1:
+            raise ValueError("the sharded step supports one parameter group")
+        ps = self.param_groups[0]["params"]
+        sizes = [p.numel() for p in ps]
+        ranges, S, padded = flat_shard_ranges(sizes, self.world, self.rank)
+        dev = ps[0].device
+        self.flat = torch.zeros(padded, dtype=torch.float32, device=dev)
+        off = 0
+        for p, n in zip(ps, sizes):
+            self.flat[off:off + n].copy_(p.data.view(-1))
+            p.data = self.flat[off:off + n].view(p.shape)
+            off += n
+        self.slice_len = S
+        self.ranges = ranges
+        for p, (lo, hi) in zip(ps, ranges):
+            st = self.state[p]
+            m, n = view_2d(p.shape)
+            st["quad"] = torch.zeros(max(hi - lo, 1), 4, device=dev, dtype=torch.float32)
+            st["row_factors"] = torch.zeros(3, m, device=dev, dtype=torch.float32)
+            st["col_factors"] = torch.zeros(3, n, device=dev, dtype=torch.float32)
+            st["step"] = self.T
+            st["range"] = (lo, hi)
+
+    def _slot(self, p, weight_slot=0) -> Slot:
+        s = super()._slot(p, weight_slot)
+        s.lo, s.hi = self.state[p]["range"]
+        return s
+
+    def _run_plan(self, plan: StepPlan, lr, weight_decay, t):
+        def timed(name, fn):
+            if self.phase_events is None:
+                fn()
+                return
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            self.phase_events.append((name, a, b))
+
+        plan.set_step(lr, weight_decay, t)
+        timed("factors", plan.factor_partials)
+        timed("factor_merge", lambda: self._all_reduce(plan.factor_sums()))
+        timed("finalize", plan.factor_finalize)
+        timed("stats", plan.feature_stats)
+        timed("stats_merge", lambda: self._all_reduce(plan.stat_sums()))
+        timed("apply", plan.apply)
+        timed("param_gather", self._gather)
+
+    def _nccl(self) -> bool:
+        return dist.get_backend(self.pg) == "nccl"
+
+    def _all_reduce(self, t):
+        if self._nccl():
+            dist.all_reduce(t, group=self.pg)
+        else:   # gloo (tests, several ranks on one device): stage through the host
+            h = t.cpu()
+            dist.all_reduce(h, group=self.pg)
+            t.copy_(h)
+
+    def _gather(self):
+        S = self.slice_len
+        local = self.flat[self.rank * S:(self.rank + 1) * S]
+        if self._nccl():
+            # in place: input is this rank's slice of the output arena
+            dist.all_gather_into_tensor(self.flat, local, group=self.pg)
+        else:
+            chunks = [torch.empty(S, dtype=torch.float32) for _ in range(self.world)]
+            dist.all_gather(chunks, local.cpu(), group=self.pg)
+            self.flat.copy_(torch.cat(chunks).to(self.flat.device))
+
+    def local_state_bytes(self) -> int:
+        return sum(int(st["quad"].numel()) * 4 for st in self.state.values() if "quad" in st)

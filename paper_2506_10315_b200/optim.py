@@ -163,14 +163,15 @@ class LearnedOptimizer(torch.optim.Optimizer):
             self._before_apply(gi, plan, params, loss)
             self._run_plan(plan, lr, group["weight_decay"], self.T + 1)
             launched.append((plan, params))
+        self._pending = launched
+        self._last = launched
+        if self.check_errors:
+            self.check()   # raises before the counter moves, like opt_step
         self.T += 1
         for group in self.param_groups:
             for p in group["params"]:
                 if p in self.state and "quad" in self.state[p]:
                     self.state[p]["step"] = self.T
-        self._pending = launched
-        if self.check_errors:
-            self.check()
         return loss
 
     def _before_apply(self, gi, plan, params, loss):
@@ -204,7 +205,8 @@ class LearnedOptimizer(torch.optim.Optimizer):
 
     def check(self):
         """Surface device-side errors of the last step (synchronizes)."""
-        for plan, params in getattr(self, "_pending", []):
+        pending, self._pending = getattr(self, "_pending", []), []
+        for plan, params in pending:
             st, _ = plan.status()
             for j, s in enumerate(st):
                 if s & _lib.LOPT_STATUS_NONFINITE_GRAD:
@@ -213,7 +215,6 @@ class LearnedOptimizer(torch.optim.Optimizer):
                 if s & _lib.LOPT_STATUS_NONFINITE_PARAM:
                     raise UpdateOverflowError(
                         f"non-finite parameters after fused step {self._name(params[j])!r}")
-        self._pending = []
 
     def _name(self, p):
         for gi, group in enumerate(self.param_groups):
@@ -225,7 +226,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
     def max_abs_updates(self):
         """UpdateReport.max_abs_update per stepped tensor of the last step."""
         out = []
-        for plan, _ in getattr(self, "_pending", []) or []:
+        for plan, _ in getattr(self, "_last", []):
             out.extend(plan.status()[1].tolist())
         return out
 

@@ -1,0 +1,159 @@
+"""World-size-2 gloo tests of the sharded step's partition and merge algebra
+(paper_2506_10315_b200/dist.py), on CPU with the oracle as the per-shard
+compute -- the same checks the reference runs on its simulated strategies
+(pkg/tests/test_distsim.py:126-167), here over real torch.distributed
+collectives: flat-arena element ranges, f64 factor-sum all-reduce, f64
+feature-sum all-reduce, parameter all-gather, result == single device."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import F32, ROOT
+
+SHAPES = [(16, 98), (16,), (10, 16), (10,), (33, 70), (1, 130), (7,)]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, kind_name, out_q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2506_10315_b200.dist import flat_shard_ranges
+    from paper_2506_10315_b200.optim import view_2d
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        kind = O.KIND_BY_NAME[kind_name]
+        rng = np.random.default_rng(0)
+        shapes2 = [view_2d(s) for s in SHAPES]
+        params = [(rng.standard_normal(s) * 0.05).astype(F32) for s in shapes2]
+        states = [O.OState.zeros(*s) for s in shapes2]
+        for _ in range(2):   # warm the accumulators identically on every rank
+            for j, s in enumerate(shapes2):
+                states[j] = O.state_step(states[j], (rng.standard_normal(s) * 1e-2).astype(F32))
+        grads = [(rng.standard_normal(s) * 1e-2).astype(F32) for s in shapes2]
+        w = O.random_weights(39 if kind == O.SMALL_FC_LOPT else 29, seed=0)
+        sizes = [m * n for m, n in shapes2]
+        ranges, S, padded = flat_shard_ranges(sizes, world, rank)
+        flat_out = np.zeros(padded, F32)
+        mism = 0
+        factor_mism = 0
+        off = 0
+        for j, ((m, n), (lo, hi)) in enumerate(zip(shapes2, ranges)):
+            g = grads[j]
+            s = states[j]
+            # single-device reference for this tensor
+            s_ref = O.state_step(s, g)
+            ref_out, _, ref_sumsq = O.step_fused(params[j], g, s_ref, w, kind)
+            # phase 0: f64 partial row/column sums over the local range
+            idx = np.arange(lo, hi, dtype=np.int64)
+            g2 = np.square(g.ravel()[lo:hi], dtype=np.float64)
+            fs = np.concatenate([np.bincount(idx // n, weights=g2, minlength=m),
+                                 np.bincount(idx % n, weights=g2, minlength=n)]).astype(np.float64)
+            t = torch.from_numpy(fs)
+            dist.all_reduce(t)
+            fs = t.numpy()
+            s2 = s.copy()
+            row_mean, col_mean = (fs[:m] / n).astype(F32), (fs[m:] / m).astype(F32)
+            for i in range(3):
+                b = F32(O.DEFAULT_BETAS[4 + i])
+                s2.r[i] = b * s.r[i] + (F32(1.0) - b) * row_mean
+                s2.c[i] = b * s.c[i] + (F32(1.0) - b) * col_mean
+                factor_mism += int(np.count_nonzero(s2.r[i] != s_ref.r[i]))
+                factor_mism += int(np.count_nonzero(s2.c[i] != s_ref.c[i]))
+                if factor_mism:
+                    print("factor mismatch", rank, j, i, s2.r[i][:4], s_ref.r[i][:4], fs[:4], flush=True)
+            s2.M = [a.copy() for a in s_ref.M]   # element-wise, identical by construction
+            s2.V = s_ref.V.copy()
+            s2.t = s_ref.t
+            # phase 1: f64 feature sums over the local range, merged
+            if hi > lo:
+                part, _ = O.fused_stats(params[j], g, s2, kind, lo=lo, hi=hi)
+            else:
+                part = np.zeros(39 if kind == O.SMALL_FC_LOPT else 29)
+            t = torch.from_numpy(np.ascontiguousarray(part))
+            dist.all_reduce(t)
+            sumsq = t.numpy()
+            np.testing.assert_allclose(sumsq, ref_sumsq, rtol=1e-12)
+            # phase 2 on the local range, into the flat arena
+            out = params[j].copy()
+            if hi > lo:
+                O.fused_apply(params[j], g, s2, w, kind, sumsq, m * n, lo=lo, hi=hi, out=out)
+            flat_out[off + lo:off + hi] = out.ravel()[lo:hi]
+            off += m * n
+        # parameter gather: every rank contributes its slice of the arena
+        local = torch.from_numpy(flat_out[rank * S:(rank + 1) * S].copy())
+        chunks = [torch.empty(S) for _ in range(world)]
+        dist.all_gather(chunks, local)
+        full = torch.cat(chunks).numpy()
+        off = 0
+        for j, (m, n) in enumerate(shapes2):
+            s_ref = O.state_step(states[j], grads[j])
+            ref_out, _, _ = O.step_fused(params[j], grads[j], s_ref, w, kind)
+            mism += int(np.count_nonzero(full[off:off + m * n] != ref_out.ravel()))
+            off += m * n
+        out_q.put((rank, mism + factor_mism, [(lo, hi) for lo, hi in ranges]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind_name", ["small_fc_lopt", "velo_mlp"])
+def test_sharded_step_equals_single_device_gloo_world2(oracle, kind_name):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind_name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, mism, ranges in results:
+        assert mism == 0, (rank, mism)
+    # the two ranks' ranges tile every tensor exactly once
+    by_rank = {r: rg for r, _, rg in results}
+    from paper_2506_10315_b200.optim import view_2d
+
+    for j, s in enumerate(SHAPES):
+        m, n = view_2d(s)
+        covered = sum(hi - lo for lo, hi in (by_rank[0][j], by_rank[1][j]))
+        assert covered == m * n
+
+
+def test_flat_shard_ranges_partition():
+    from paper_2506_10315_b200.dist import flat_shard_ranges, owner_plan, worker_ranges
+
+    sizes = [590592, 768, 151296, 7, 1, 2359296, 3]
+    for world in (1, 2, 3, 8):
+        total = 0
+        for r in range(world):
+            ranges, S, padded = flat_shard_ranges(sizes, world, r)
+            assert padded % world == 0 and S * world == padded
+            total += sum(hi - lo for lo, hi in ranges)
+            for (lo, hi), n in zip(ranges, sizes):
+                assert 0 <= lo <= hi <= n
+        assert total == sum(sizes)
+    r = worker_ranges(10, 27, 4)
+    assert r[0][0] == 10 and r[-1][1] == 27
+    assert max(b - a for a, b in r) - min(b - a for a, b in r) <= 1
+    owners = owner_plan([5, 100, 7, 60, 60], 2)
+    assert owners[1] == 0 and sorted(set(owners)) == [0, 1]

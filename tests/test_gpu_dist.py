@@ -1,0 +1,102 @@
+"""The sharded optimizer (paper_2506_10315_b200.dist) on the GPU: two ranks
+share the box's single B200 (gloo carries the collectives; on a multi-GPU node
+the same code runs NCCL), and the sharded step must equal the single-GPU
+step -- bitwise in strict mode, within the fp32 tolerance in fast mode."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(256, 192), (256,), (96, 256), (96,), (33, 70), (1, 130), (7,), (1, 1, 64)]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _init(seed=0):
+    rng = np.random.default_rng(seed)
+    init = [np.asarray(rng.standard_normal(s) * 0.05, np.float32) for s in SHAPES]
+    grads = [[np.asarray(rng.standard_normal(s) * 1e-2, np.float32) for s in SHAPES]
+             for _ in range(3)]
+    return init, grads
+
+
+def _worker(rank, world, port, mode, fs, q):
+    import sys
+    import traceback
+
+    sys.path.insert(0, ROOT)
+    try:
+        import torch
+        import torch.distributed as dist
+
+        import paper_2506_10315_b200 as P
+        from paper_2506_10315_b200.dist import ShardedLearnedOptimizer
+
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        init, grads = _init()
+        params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+        opt = ShardedLearnedOptimizer(params, feature_set=fs, mode=mode, weight_decay=0.01)
+        for gs in grads:
+            for p, g in zip(params, gs):
+                p.grad = torch.from_numpy(g).cuda()
+            opt.step()
+        torch.cuda.synchronize()
+        out = [p.detach().cpu().numpy().copy() for p in params]
+        q.put((rank, out, opt.local_state_bytes()))
+        dist.destroy_process_group()
+    except Exception:
+        q.put((rank, traceback.format_exc(), 0))
+
+
+@pytest.mark.parametrize("mode,fs", [("strict", "small_fc_lopt"), ("fast", "velo_mlp"),
+                                     ("fast", "small_fc_lopt")])
+def test_sharded_equals_single_gpu(mode, fs):
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_2506_10315_b200 as P
+
+    init, grads = _init()
+    params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    opt = P.LearnedOptimizer(params, feature_set=fs, mode=mode, weight_decay=0.01)
+    for gs in grads:
+        for p, g in zip(params, gs):
+            p.grad = torch.from_numpy(g).cuda()
+        opt.step()
+    single = [p.detach().cpu().numpy() for p in params]
+    full_state = sum(int(opt.state[p]["quad"].numel()) * 4 for p in params)
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, fs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, out, state_bytes in res:
+        assert not isinstance(out, str), out
+        # optimizer state is sharded: each rank holds about half
+        assert state_bytes <= full_state // 2 + 4 * 4 * len(SHAPES)
+        for a, b in zip(out, single):
+            if mode == "strict":
+                assert a.tobytes() == b.tobytes()
+            else:
+                err = np.abs(a.astype(np.float64) - b) / (1 + np.abs(b))
+                assert err.max() <= 1e-6, err.max()

@@ -189,6 +189,9 @@ def test_nonfinite_gradient_raises_and_changes_nothing(P):
         opt.step()
     assert torch.equal(a.detach(), torch.ones(2, 2, device="cuda"))
     assert torch.equal(b.detach(), torch.ones(3, 3, device="cuda"))
+    for p in (a, b):   # no accumulator was committed either
+        st = opt.state[p]
+        assert not st["quad"].any() and not st["row_factors"].any() and not st["col_factors"].any()
 
 
 def test_decay_runs_after_update_exactly(P):
