@@ -41,23 +41,73 @@ struct __align__(128) ApplySmem {
 struct TileLoad {
   int j;
   bool valid;
-  int64_t e;
+  int64_t e, a, b;   // flat element and its (row, column)
   float w, g;
   float4 s;
 };
 
-__device__ __forceinline__ void load_tile(const DevicePlan &P, int &jwalk, int64_t t, int row,
+// Walks a warpgroup's contiguous tile range: current tensor, tile origin
+// (row a0, column b0) advanced incrementally from tile to tile.
+struct TileWalker {
+  int j = -1;
+  int64_t next_tile0 = -1, tile0 = 0, lo = 0, hi = 0, n = 1, t = -2, a0 = 0, b0 = 0;
+};
+
+__device__ __forceinline__ void walk_to(const DevicePlan &P, TileWalker &W, int64_t t) {
+  if (W.j < 0 || t >= W.next_tile0) {
+    int j = W.j < 0 ? 0 : W.j;
+    while (j + 1 < P.count && P.tensors[j + 1].tile0 <= t) j++;
+    const TensorDesc *T = P.tensors + j;
+    W.j = j;
+    W.tile0 = T->tile0;
+    W.lo = T->lo;
+    W.hi = T->hi;
+    W.n = T->n;
+    W.next_tile0 = j + 1 < P.count ? P.tensors[j + 1].tile0 : INT64_MAX;
+    W.t = -2;
+  }
+  const int64_t e0 = W.lo + (t - W.tile0) * kTile;
+  if (t == W.t + 1 && W.n >= kTile) {
+    W.b0 += kTile;
+    if (W.b0 >= W.n) {
+      W.b0 -= W.n;
+      W.a0++;
+      if (W.b0 >= W.n) {   // only when n < 2*kTile... keep exact
+        W.a0 += W.b0 / W.n;
+        W.b0 %= W.n;
+      }
+    }
+  } else {
+    W.a0 = e0 / W.n;
+    W.b0 = e0 - W.a0 * W.n;
+  }
+  W.t = t;
+}
+
+__device__ __forceinline__ void load_tile(const DevicePlan &P, TileWalker &W, int64_t t, int row,
                                           TileLoad &L) {
-  while (jwalk + 1 < P.count && P.tensors[jwalk + 1].tile0 <= t) jwalk++;
-  const TensorDesc *T = P.tensors + jwalk;
-  const int64_t lo = T->lo;
-  L.j = jwalk;
-  L.e = lo + (t - T->tile0) * kTile + row;
-  L.valid = L.e < T->hi;
+  walk_to(P, W, t);
+  const TensorDesc *T = P.tensors + W.j;
+  L.j = W.j;
+  L.e = W.lo + (t - W.tile0) * kTile + row;
+  L.valid = L.e < W.hi;
+  int64_t b = W.b0 + row, a = W.a0;
+  if (b >= W.n) {
+    if (W.n >= kTile) {
+      b -= W.n;
+      a++;
+    } else {
+      const uint32_t q = (uint32_t)b / (uint32_t)W.n;
+      a += q;
+      b -= (int64_t)q * W.n;
+    }
+  }
+  L.a = a;
+  L.b = b;
   if (L.valid) {
     L.w = __ldg(T->theta + L.e);
     L.g = __ldg(T->grad + L.e);
-    L.s = __ldg(T->state + (L.e - lo));
+    L.s = __ldg(T->state + (L.e - W.lo));
   } else {
     L.w = L.g = 0.0f;
     L.s = make_float4(0.f, 0.f, 0.f, 0.f);
