@@ -96,6 +96,8 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
     if (t.m < 1 || t.n < 1) return LOPT_ERR_SHAPE;
     if (t.lo < 0 || t.hi < t.lo || t.hi > t.m * t.n) return LOPT_ERR_SHAPE;
     if (t.n > (int64_t)1 << 31 || t.m > (int64_t)1 << 40) return LOPT_ERR_SHAPE;
+    // the tensor-core kernel indexes elements with 32-bit integers
+    if (cfg->mode == LOPT_MODE_FAST && t.m * t.n >= ((int64_t)1 << 31)) return LOPT_ERR_UNSUPPORTED;
     if (!t.theta || !t.grad || !t.row_factors || !t.col_factors) return LOPT_ERR_INVALID;
     if (t.hi > t.lo && !t.state) return LOPT_ERR_INVALID;
     if ((reinterpret_cast<uintptr_t>(t.state) & 15) != 0) return LOPT_ERR_INVALID;

@@ -212,7 +212,10 @@ __global__ void stats_reduce_fast_kernel(DevicePlan P) {
 // ---------------------------------------------------------------------------
 // host launchers
 
-int fast_supported(const DevicePlan &P) { return P.h1 == 32 && P.h2 == 32 ? 1 : 0; }
+// The tensor-core apply kernel indexes with 32-bit integers.
+int fast_supported(const DevicePlan &P) {
+  return P.h1 == 32 && P.h2 == 32 && P.n_tiles < ((int64_t)1 << 31) ? 1 : 0;
+}
 int64_t fast_stat_chunk() { return kFastStatChunk; }
 int64_t fast_apply_chunk() { return kTile; }
 size_t prep_image_bytes() { return sizeof(PrepImage); }
