@@ -28,6 +28,7 @@ void launch_fast_apply(const DevicePlan &P, cudaStream_t s);
 int64_t fast_stat_chunk();
 int64_t fast_apply_chunk();
 size_t prep_image_bytes();
+int64_t factor_strip_cols();
 }  // namespace lopt
 
 using namespace lopt;
@@ -142,7 +143,7 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
           p->fitems.push_back(it);
         }
       } else {
-        const int64_t strip = 1024;
+        const int64_t strip = factor_strip_cols();
         d.nstrips = (int32_t)((t.n + strip - 1) / strip);
         const int64_t width = std::min<int64_t>(t.n, strip);
         int64_t R = kFactorTileElems / width;

@@ -14,86 +14,94 @@ namespace lopt {
 
 constexpr int kFactorThreads = 256;
 constexpr int kFactorWarps = kFactorThreads / 32;
-constexpr int kStripCols = 1024;     // 32 columns per lane
+constexpr int kStripCols = 512;      // columns per tile strip (16 per lane)
 
-// One tile per CTA: rows [a0, a1) x columns [b0, b1).  Warps own rows (w, w+8,
-// ...), lanes own columns (lane + 32k), so every g row segment is read
-// coalesced exactly once.  Vector tensors (n == 1) take the thread-per-row path.
-__global__ void __launch_bounds__(kFactorThreads)
-factor_partials_kernel(DevicePlan P) {
-  const FactorItem it = P.factor_items[blockIdx.x];
-  const TensorDesc T = P.tensors[it.tensor];
+__device__ __forceinline__ void flag_nonfinite(const DevicePlan &P, int tensor) {
+  atomicOr(&P.status[tensor], LOPT_STATUS_NONFINITE_GRAD);
+  atomicOr(P.abort_flag, 1u);
+  *P.grad_flag = 1.0;
+}
+
+// Loads one row segment of the strip into v[16]: VEC lanes own 4 consecutive
+// columns per 128-column slab (16-byte loads), otherwise 1 column per 32.
+template <bool VEC>
+__device__ __forceinline__ void load_row(const float *grow, int64_t b0, int64_t b1, int lane,
+                                         float (&v)[16]) {
+  if (VEC) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int64_t b = b0 + 4 * lane + 128 * k;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (b < b1) x = __ldg(reinterpret_cast<const float4 *>(grow + b));
+      v[4 * k + 0] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const int64_t b = b0 + lane + 32 * k;
+      v[k] = b < b1 ? __ldg(grow + b) : 0.0f;
+    }
+  }
+}
+
+template <bool VEC>
+__device__ __forceinline__ int64_t col_of(int64_t b0, int lane, int k) {
+  return VEC ? b0 + 4 * lane + 128 * (k >> 2) + (k & 3) : b0 + lane + 32 * k;
+}
+
+// One tile per CTA: rows [a0, a1) x columns [b0, b1), b1 - b0 <= 512.  Warp w
+// owns rows a0+w, a0+w+8, ... and processes two rows per step so 2 x 16 loads
+// are in flight per lane; lanes own fixed columns, so column partials stay in
+// registers (f64) and are combined across warps once, in warp order.  The
+// element-range mask of a sharded plan is applied only on rows that straddle
+// [lo, hi).  A non-finite gradient shows up as a non-finite row sum.
+template <bool VEC>
+__device__ void factor_tile(const DevicePlan &P, const FactorItem &it, const TensorDesc &T) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ double colbuf[kStripCols];
-  __shared__ double wsum[kFactorWarps];
   __shared__ uint32_t bad_s;
   if (tid == 0) bad_s = 0;
-  __syncthreads();
-  uint32_t bad = 0;
-  const float *g = T.grad;
-
-  if (T.n == 1) {
-    // vector (m,1): row sum of row a is g[a]^2; the single column sums all rows
-    double acc = 0.0;
-    for (int64_t a = it.a0 + tid; a < it.a1; a += kFactorThreads) {
-      double sq = 0.0;
-      if (a >= T.lo && a < T.hi) {
-        const float v = g[a];
-        bad |= !isfinite(v);
-        sq = (double)v * (double)v;
-      }
-      T.rowpart[a] = sq;   // strip 0
-      acc += sq;
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) wsum[warp] = acc;
-    if (bad) atomicOr(&bad_s, 1u);
-    __syncthreads();
-    if (tid == 0) {
-      double s = 0.0;
-      for (int w = 0; w < kFactorWarps; w++) s += wsum[w];
-      T.colpart[it.rowblock] = s;
-      if (bad_s) {
-        atomicOr(&P.status[it.tensor], LOPT_STATUS_NONFINITE_GRAD);
-        atomicOr(P.abort_flag, 1u);
-        *P.grad_flag = 1.0;
-      }
-    }
-    return;
-  }
-
-  constexpr int K = kStripCols / 32;
-  double colacc[K];
+  double colacc[16];
 #pragma unroll
-  for (int k = 0; k < K; k++) colacc[k] = 0.0;
+  for (int k = 0; k < 16; k++) colacc[k] = 0.0;
   const int64_t n = T.n;
-  for (int64_t a = it.a0 + warp; a < it.a1; a += kFactorWarps) {
-    const float *grow = g + a * n;
-    const int64_t rowbase = a * n;
-    double rowp = 0.0;
+  bool bad = false;
+  for (int64_t a = it.a0 + warp; a < it.a1; a += 2 * kFactorWarps) {
+    const int64_t a2 = a + kFactorWarps;
+    const bool has2 = a2 < it.a1;
+    float v[2][16];
+    load_row<VEC>(T.grad + a * n, it.b0, it.b1, lane, v[0]);
+    if (has2) load_row<VEC>(T.grad + a2 * n, it.b0, it.b1, lane, v[1]);
 #pragma unroll
-    for (int k = 0; k < K; k++) {
-      const int64_t b = it.b0 + lane + 32 * k;
-      if (b < it.b1) {
-        const int64_t e = rowbase + b;
-        if (e >= T.lo && e < T.hi) {
-          const float v = grow[b];
-          bad |= !isfinite(v);
-          const double sq = (double)v * (double)v;
-          colacc[k] += sq;
-          rowp += sq;
+    for (int r = 0; r < 2; r++) {
+      if (r == 1 && !has2) break;
+      const int64_t row = r == 0 ? a : a2;
+      const bool full = row * n >= T.lo && (row + 1) * n <= T.hi;
+      double rowp = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; k++) {
+        double sq = (double)v[r][k] * (double)v[r][k];
+        if (!full) {
+          const int64_t e = row * n + col_of<VEC>(it.b0, lane, k);
+          if (e < T.lo || e >= T.hi) sq = 0.0;
         }
+        colacc[k] += sq;
+        rowp += sq;
+      }
+      rowp = warp_sum(rowp);
+      if (lane == 0) {
+        T.rowpart[(int64_t)it.strip * T.m + row] = rowp;
+        bad |= !isfinite(rowp);
       }
     }
-    rowp = warp_sum(rowp);
-    if (lane == 0) T.rowpart[(int64_t)it.strip * T.m + a] = rowp;
   }
   // combine the warps' column partials in warp order
+  __syncthreads();
   for (int w = 0; w < kFactorWarps; w++) {
     if (warp == w) {
 #pragma unroll
-      for (int k = 0; k < K; k++) {
-        const int j = lane + 32 * k;
+      for (int k = 0; k < 16; k++) {
+        const int j = (int)(col_of<VEC>(0, lane, k));
         colbuf[j] = (w == 0) ? colacc[k] : colbuf[j] + colacc[k];
       }
     }
@@ -104,10 +112,55 @@ factor_partials_kernel(DevicePlan P) {
     T.colpart[(int64_t)it.rowblock * n + it.b0 + j] = colbuf[j];
   if (bad) atomicOr(&bad_s, 1u);
   __syncthreads();
-  if (tid == 0 && bad_s) {
-    atomicOr(&P.status[it.tensor], LOPT_STATUS_NONFINITE_GRAD);
-    atomicOr(P.abort_flag, 1u);
-    *P.grad_flag = 1.0;
+  if (tid == 0 && bad_s) flag_nonfinite(P, it.tensor);
+}
+
+// Vector (m, 1): the row sum of row a is g[a]^2; the single column sums all
+// rows.  Four rows per thread per step, loads first.
+__device__ void factor_vector(const DevicePlan &P, const FactorItem &it, const TensorDesc &T) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double wsum[kFactorWarps];
+  __shared__ uint32_t bad_s;
+  if (tid == 0) bad_s = 0;
+  __syncthreads();
+  double acc = 0.0;
+  for (int64_t a = it.a0 + tid; a < it.a1; a += 4 * kFactorThreads) {
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t r = a + u * kFactorThreads;
+      v[u] = (r < it.a1 && r >= T.lo && r < T.hi) ? __ldg(T.grad + r) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const int64_t r = a + u * kFactorThreads;
+      if (r < it.a1) {
+        const double sq = (double)v[u] * (double)v[u];
+        T.rowpart[r] = sq;   // strip 0
+        acc += sq;
+      }
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) wsum[warp] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kFactorWarps; w++) s += wsum[w];
+    T.colpart[it.rowblock] = s;
+    if (!isfinite(s)) flag_nonfinite(P, it.tensor);
+  }
+}
+
+__global__ void __launch_bounds__(kFactorThreads, 2) factor_partials_kernel(DevicePlan P) {
+  const FactorItem it = P.factor_items[blockIdx.x];
+  const TensorDesc T = P.tensors[it.tensor];
+  if (T.n == 1) {
+    factor_vector(P, it, T);
+  } else if ((T.n & 3) == 0 && (reinterpret_cast<uintptr_t>(T.grad) & 15) == 0) {
+    factor_tile<true>(P, it, T);
+  } else {
+    factor_tile<false>(P, it, T);
   }
 }
 
@@ -233,9 +286,10 @@ __global__ void __launch_bounds__(256) factor_means_kernel(DevicePlan P) {
   }
 }
 
-}  // namespace lopt
+// ---------------------------------------------------------------------------
+// host launchers
 
-namespace lopt {
+int64_t factor_strip_cols() { return kStripCols; }
 
 void launch_factor_partials(const DevicePlan &P, cudaStream_t s) {
   if (P.n_factor_items > 0) factor_partials_kernel<<<P.n_factor_items, kFactorThreads, 0, s>>>(P);

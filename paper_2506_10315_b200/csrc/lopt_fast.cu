@@ -150,22 +150,54 @@ __global__ void __launch_bounds__(kFastStatThreads) stats_fast_kernel(DevicePlan
 #pragma unroll
   for (int k = 0; k < NE; k++) acc[k] = 0.0f;
   const bool adv = P.state_advanced != 0;
-  for (int64_t e = it.e0 + threadIdx.x; e < it.e1; e += kFastStatThreads) {
-    FastIn x;
-    x.w = __ldg(T.theta + e);
-    advance(__ldg(T.grad + e), T.state[e - T.lo], adv, P.beta, x);
+  // four consecutive elements per thread per step: 16-byte loads of theta and
+  // g when the chunk is aligned, one divmod per four elements
+  const bool vec = ((it.e0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(T.theta) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(T.grad) & 15) == 0);
+  for (int64_t e = it.e0 + 4 * threadIdx.x; e < it.e1; e += 4 * kFastStatThreads) {
+    const int cnt = it.e1 - e < 4 ? (int)(it.e1 - e) : 4;
+    float w4[4], g4[4];
+    if (vec && cnt == 4) {
+      const float4 w = __ldg(reinterpret_cast<const float4 *>(T.theta + e));
+      const float4 g = __ldg(reinterpret_cast<const float4 *>(T.grad + e));
+      w4[0] = w.x; w4[1] = w.y; w4[2] = w.z; w4[3] = w.w;
+      g4[0] = g.x; g4[1] = g.y; g4[2] = g.z; g4[3] = g.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        w4[u] = u < cnt ? __ldg(T.theta + e + u) : 0.0f;
+        g4[u] = u < cnt ? __ldg(T.grad + e + u) : 0.0f;
+      }
+    }
+    float4 s4[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) s4[u] = u < cnt ? __ldg(T.state + (e + u - T.lo)) : make_float4(0.f, 0.f, 0.f, 0.f);
     int64_t a, b;
     divmod(e, T.n, inv_n, a, b);
-    const float4 rt = reinterpret_cast<const float4 *>(T.rowtab + a * kRowTab)[0];
-    const float4 ct = reinterpret_cast<const float4 *>(T.coltab + b * kRowTab)[0];
-    const float rc[3] = {rt.x, rt.y, rt.z}, cc[3] = {ct.x, ct.y, ct.z};
-    float f[16];
-    fast_features(x, rc, cc, sqmr, f);
 #pragma unroll
-    for (int k = 0; k < 16; k++) acc[k] = fmaf(f[k], f[k], acc[k]);
-    if (KIND == LOPT_VELO_MLP) {
-      const float cg = clip01(x.g);
-      acc[NE - 1] = fmaf(cg, cg, acc[NE - 1]);
+    for (int u = 0; u < 4; u++) {
+      if (u > 0) {
+        b++;
+        if (b >= T.n) {
+          b = 0;
+          a++;
+        }
+      }
+      if (u >= cnt) break;
+      FastIn x;
+      x.w = w4[u];
+      advance(g4[u], s4[u], adv, P.beta, x);
+      const float4 rt = reinterpret_cast<const float4 *>(T.rowtab + a * kRowTab)[0];
+      const float4 ct = reinterpret_cast<const float4 *>(T.coltab + b * kRowTab)[0];
+      const float rc[3] = {rt.x, rt.y, rt.z}, cc[3] = {ct.x, ct.y, ct.z};
+      float f[16];
+      fast_features(x, rc, cc, sqmr, f);
+#pragma unroll
+      for (int k = 0; k < 16; k++) acc[k] = fmaf(f[k], f[k], acc[k]);
+      if (KIND == LOPT_VELO_MLP) {
+        const float cg = clip01(x.g);
+        acc[NE - 1] = fmaf(cg, cg, acc[NE - 1]);
+      }
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
