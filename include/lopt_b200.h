@@ -136,22 +136,31 @@ int lopt_read_status(lopt_plan *plan, uint32_t *status_host, float *maxabs_host,
 int lopt_debug_ptrs(lopt_plan *plan, double **sumsq, float **factor_means);
 
 /* VeLO per-tensor hypernetwork (build-defined, no reference counterpart;
- * SURVEY.md section 8(a) row 15): one LSTM step per tensor on inputs derived
- * from that tensor's phase-1 feature sums and the step/loss features, then
- * softmax mixing of a bank of `bank_size` packed MLPs into the plan's
- * per-tensor weight slots (slot j = tensor j).  lstm_params: packed LSTM +
- * head weights (see paper_2506_10315_b200/velo.py for the layout);
- * lstm_state: (count x 2 x hidden) h|c, updated in place; bank: bank_size
- * packed MLPs; loss_feats: 2 floats {log loss, its EMA}. */
-int lopt_velo_mix(lopt_plan *plan, const float *lstm_params, float *lstm_state,
-                  const float *bank, int32_t hidden, int32_t bank_size, int32_t input_dim,
-                  int32_t reserved, const float *loss_feats);
+ * SURVEY.md section 8(a) row 15).  Runs between lopt_feature_stats (after any
+ * cross-rank stats merge) and lopt_apply: for every tensor j one LSTM step on
+ * x_j = [log(sumsq_j/count_j + 1e-5) (29) | tanh(t/x) (11) | loss features (2)],
+ * softmax over a head -> mixing weights a_j (bank_size), and the per-tensor
+ * MLP sum_k a_jk * bank_k written into weight slot j (the plan must have
+ * num_weight_sets == count and tensor j using slot j).  All pointers are
+ * device pointers: hyper = W_x (4H x 42) | W_h (4H x H) | b (4H) | W_o (K x H)
+ * | b_o (K); lstm_state = count x (h[H] | c[H]), updated in place; bank = K
+ * packed MLPs (lopt_set_weights layout); loss_feats = 2 floats; mix_out =
+ * count x K mixing weights (may be NULL).  hidden <= 64, bank_size <= 16. */
+int lopt_velo_mix(lopt_plan *plan, const float *hyper, float *lstm_state, const float *bank,
+                  const float *loss_feats, int32_t hidden, int32_t bank_size, float *mix_out,
+                  void *stream);
 
 /* Known-answer test of the tcgen05 building blocks (device pointers):
  * D[128 x 32] f32 = A[128 x K] * B[32 x K]^T, K in {16,32,48,64}; flag bit 0:
  * A staged in tensor memory (else shared memory), bit 1: fp16 operands (else bf16). */
 int lopt_selftest_umma(int32_t a_in_tmem, int32_t K, const void *A, const void *B, float *D,
                        void *stream);
+/* The strict path's expf (glibc's algorithm restated, lopt_common.cuh) over a
+ * device array, for the bitwise test against the host libm. */
+int lopt_selftest_expf(const float *x, float *y, int64_t n, void *stream);
+/* Micro-benchmark of the fast path's MMA shape: `batch` MMAs per commit,
+ * `rounds` commit/wait round trips; out[0] = SM cycles per round. */
+int lopt_probe_umma(int32_t batch, int32_t rounds, long long *out, void *stream);
 
 const char *lopt_version(void);
 int lopt_num_kernels_launched_last_step(const lopt_plan *plan);

@@ -57,6 +57,11 @@ static const float CLIP_BOUND = 0.1f;    /* features.py:82 */
 
 int lo_d_feat(int kind) { return kind == LO_SMALL_FC_LOPT ? 39 : 29; }
 
+/* libm expf over an array (what numba's np.exp on float32 calls). */
+void lo_expf_array(const float *x, float *y, int64_t n) {
+  for (int64_t i = 0; i < n; i++) y[i] = expf(x[i]);
+}
+
 /* ------------------------------------------------------------------ */
 /* numpy f64 reduction orders                                           */
 

@@ -96,6 +96,8 @@ def lib():
             ctypes.c_double, fp, i64, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
         ]
         L.lo_opt_step.restype = ctypes.c_int
+        L.lo_expf_array.argtypes = [fp, fp, i64]
+        L.lo_expf_array.restype = None
         _lib = L
     return _lib
 
@@ -221,6 +223,14 @@ def state_step(s: OState, g, betas=DEFAULT_BETAS) -> OState:
         raise OracleError(st)
     out.t = s.t + 1
     return out
+
+
+def libm_expf(x):
+    """glibc expf elementwise (the exp numba uses, engine.py:537)."""
+    x = np.ascontiguousarray(x, F32)
+    y = np.empty_like(x)
+    lib().lo_expf_array(_f(x), _f(y), x.size)
+    return y
 
 
 def factor_means(s: OState):

@@ -8,6 +8,7 @@ from .features import (FeatureSet, FeatureSetSpec, column_names, small_fc_lopt_s
                        spec_by_name, time_features, velo_mlp_spec)
 from .optim import AdafacLO_CUDA, LearnedOptimizer, OptimError, view_2d
 from .schedule import ScheduleConfig, schedule_lr
+from .velo import VeLO_CUDA, VeLOHyperNet
 from .weights import BetaConfig, LoptWeights, random_weights, zero_weights
 
 __all__ = [

@@ -33,6 +33,7 @@ EXPORTS = [
     "lopt_step", "lopt_factor_sums_ptr", "lopt_stat_sums_ptr", "lopt_status_ptr",
     "lopt_read_status", "lopt_debug_ptrs", "lopt_version",
     "lopt_num_kernels_launched_last_step", "lopt_velo_mix", "lopt_selftest_umma",
+    "lopt_probe_umma", "lopt_selftest_expf",
 ]
 
 
@@ -120,8 +121,10 @@ def lib(required: bool = True):
     L.lopt_debug_ptrs.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp)]
     L.lopt_version.restype = ctypes.c_char_p
     L.lopt_num_kernels_launched_last_step.argtypes = [vp]
-    L.lopt_velo_mix.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp]
+    L.lopt_velo_mix.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, vp]
     L.lopt_selftest_umma.argtypes = [i32, i32, vp, vp, vp, vp]
+    L.lopt_probe_umma.argtypes = [i32, i32, vp, vp]
+    L.lopt_selftest_expf.argtypes = [vp, vp, ctypes.c_int64, vp]
     for name in EXPORTS:
         f = getattr(L, name)
         if name != "lopt_version":

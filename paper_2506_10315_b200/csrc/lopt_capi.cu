@@ -29,6 +29,8 @@ int64_t fast_stat_chunk();
 int64_t fast_apply_chunk();
 size_t prep_image_bytes();
 int64_t factor_strip_cols();
+int launch_velo_mix(const DevicePlan &P, const float *hyper, float *lstm_state, const float *bank,
+                    const float *loss_feats, int H, int K, float *mix_out, cudaStream_t s);
 }  // namespace lopt
 
 using namespace lopt;
@@ -491,12 +493,17 @@ int lopt_debug_ptrs(lopt_plan *p, double **sumsq, float **factor_means) {
   return LOPT_OK;
 }
 
-int lopt_velo_mix(lopt_plan *p, const float *lstm_params, float *lstm_state, const float *bank,
-                  int32_t hidden, int32_t bank_size, int32_t input_dim, int32_t reserved,
-                  const float *loss_feats) {
-  (void)p; (void)lstm_params; (void)lstm_state; (void)bank; (void)hidden; (void)bank_size;
-  (void)input_dim; (void)reserved; (void)loss_feats;
-  return LOPT_ERR_UNSUPPORTED;
+int lopt_velo_mix(lopt_plan *p, const float *hyper, float *lstm_state, const float *bank,
+                  const float *loss_feats, int32_t hidden, int32_t bank_size, float *mix_out,
+                  void *stream) {
+  if (!p || !p->ws || !hyper || !lstm_state || !bank || !loss_feats) return LOPT_ERR_INVALID;
+  if (p->cfg.num_weight_sets != (int32_t)p->tensors.size()) return LOPT_ERR_INVALID;
+  for (size_t j = 0; j < p->tensors.size(); j++)
+    if (p->tensors[j].weight_slot != (int32_t)j) return LOPT_ERR_INVALID;
+  const int st = launch_velo_mix(p->dp, hyper, lstm_state, bank, loss_feats, hidden, bank_size,
+                                 mix_out, (cudaStream_t)stream);
+  if (st == LOPT_OK) p->launches_last_step += 1;
+  return st;
 }
 
 int lopt_num_kernels_launched_last_step(const lopt_plan *p) {

@@ -77,7 +77,78 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(int a_in_tmem, int f
   if (warp == 0) tc::tmem_dealloc(base, 128);
 }
 
+// Latency / throughput probe of the MMA shape the fast path uses
+// (M=128, N=32, K=16, f16, A in TMEM): `batch` MMAs per commit, `rounds`
+// commit->wait round trips, cycles reported per round in out[0].
+__global__ void __launch_bounds__(128) umma_probe_kernel(int batch, int rounds, int N, int a_smem,
+                                                         long long *out) {
+  __shared__ __align__(1024) uint16_t Bs[256 * 16];
+  __shared__ __align__(1024) uint16_t As[128 * 16];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tbase;
+  const int t = threadIdx.x, warp = t >> 5;
+  for (int i = t; i < 256 * 16; i += 128) Bs[i] = 0x3C00;
+  for (int i = t; i < 128 * 16; i += 128) As[i] = 0x3C00;
+  if (warp == 0) {
+    tc::tmem_alloc(&tbase, 512);
+    tc::tmem_relinquish();
+  }
+  if (t == 0) {
+    tc::mbar_init(&mbar, 1);
+    tc::mbar_fence_init();
+  }
+  tc::fence_proxy_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t base = tbase;
+  if (t == 0) {
+    const uint32_t idesc = tc::idesc_f16_f32(128, N);
+    const uint64_t bdesc = tc::smem_desc_kmajor(tc::smem_u32(Bs), N * 16, 128);
+    const uint64_t adesc = tc::smem_desc_kmajor(tc::smem_u32(As), 2048, 128);
+    long long t0 = clock64();
+    for (int r = 0; r < rounds; r++) {
+      for (int b = 0; b < batch; b++) {
+        if (a_smem) tc::mma_ss(base, adesc, bdesc, idesc, b > 0);
+        else tc::mma_ts(base, base + 256, bdesc, idesc, b > 0);
+      }
+      tc::mma_commit(&mbar);
+      tc::mbar_wait(&mbar, r & 1);
+    }
+    long long t1 = clock64();
+    out[0] = (t1 - t0) / rounds;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(base, 512);
+}
+
+__global__ void expf_selftest_kernel(const float *x, float *y, int64_t n) {
+  __shared__ uint64_t tab[32];
+  if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = glibc_expf(x[i], tab);
+}
+
 }  // namespace lopt
+
+extern "C" int lopt_selftest_expf(const float *x, float *y, int64_t n, void *stream) {
+  if (!x || !y || n < 0) return LOPT_ERR_INVALID;
+  lopt::expf_selftest_kernel<<<296, 256, 0, (cudaStream_t)stream>>>(x, y, n);
+  return cudaGetLastError() == cudaSuccess ? LOPT_OK : LOPT_ERR_CUDA;
+}
+
+extern "C" int lopt_probe_umma(int32_t batch, int32_t rounds, long long *out, void *stream) {
+  // batch: low 16 bits = MMAs per commit; bits 16..27 = N (default 32);
+  // bit 28 = A from shared memory
+  const int b = batch & 0xFFFF, N = (batch >> 16) & 0xFFF ? (batch >> 16) & 0xFFF : 32;
+  const int a_smem = (batch >> 28) & 1;
+  if (N < 16 || N > 256 || N % 16) return LOPT_ERR_INVALID;
+  lopt::umma_probe_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(b, rounds, N, a_smem, out);
+  return cudaGetLastError() == cudaSuccess ? LOPT_OK : LOPT_ERR_CUDA;
+}
 
 extern "C" int lopt_selftest_umma(int32_t a_in_tmem, int32_t K, const void *A, const void *B,
                                   float *D, void *stream) {

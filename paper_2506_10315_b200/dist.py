@@ -109,23 +109,16 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         s.lo, s.hi = self.state[p]["range"]
         return s
 
-    def _run_plan(self, plan: StepPlan, lr, weight_decay, t):
-        def timed(name, fn):
-            if self.phase_events is None:
-                fn()
-                return
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            fn()
-            b.record()
-            self.phase_events.append((name, a, b))
-
+    def _run_plan(self, plan: StepPlan, lr, weight_decay, t, gi, params):
+        timed = self._timed
         plan.set_step(lr, weight_decay, t)
         timed("factors", plan.factor_partials)
         timed("factor_merge", lambda: self._all_reduce(plan.factor_sums()))
         timed("finalize", plan.factor_finalize)
         timed("stats", plan.feature_stats)
         timed("stats_merge", lambda: self._all_reduce(plan.stat_sums()))
+        if self._after_stats is not None:
+            timed("hypernet", lambda: self._after_stats(gi, plan, params))
         timed("apply", plan.apply)
         timed("param_gather", self._gather)
 
@@ -153,3 +146,32 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
 
     def local_state_bytes(self) -> int:
         return sum(int(st["quad"].numel()) * 4 for st in self.state.values() if "quad" in st)
+
+
+def _sharded_velo_cls():
+    from .velo import VeLOHyperNet, _VeLOMixin
+
+    class ShardedVeLO(_VeLOMixin, ShardedLearnedOptimizer):
+        """VeLO_CUDA sharded by element ranges: every rank runs the (tiny)
+        hypernetwork on the merged statistics, so all ranks mix identical
+        per-tensor MLPs."""
+
+        def __init__(self, params, lr=1.0, weight_decay=0.0, *, hypernet=None, **kw):
+            kw.pop("feature_set", None)
+            hn = hypernet or VeLOHyperNet()
+            super().__init__(params, lr=lr, weight_decay=weight_decay, feature_set="velo_mlp",
+                             weights=hn.bank[0], **kw)
+            self._velo_init(hn)
+
+        def step(self, closure=None, loss=None):
+            if closure is not None:
+                with torch.enable_grad():
+                    loss = closure()
+            self._set_loss(loss)
+            return super().step(loss=loss)
+
+    return ShardedVeLO
+
+
+def ShardedVeLO(*args, **kw):
+    return _sharded_velo_cls()(*args, **kw)

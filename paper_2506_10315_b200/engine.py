@@ -160,7 +160,10 @@ class StepPlan:
         args = _lib.lopt_step_args()
         args.lr = float(lr)
         args.weight_decay = float(weight_decay)
-        tf = time_features(t, self.spec)
+        # tanh(t/x) for all 11 horizons: the small_fc_lopt columns
+        # (features.py:125-130) and the VeLO hypernetwork inputs; the
+        # VELO_MLP per-element kernels ignore them
+        tf = time_features(t, small_fc_lopt_spec())
         for k in range(11):
             args.time_features[k] = float(tf[k])
         args.t = int(t)

@@ -160,8 +160,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
                 continue
             lr = lr_sched if lr_sched is not None else group["lr"]
             plan = self._plan_for_group(gi, params)
-            self._before_apply(gi, plan, params, loss)
-            self._run_plan(plan, lr, group["weight_decay"], self.T + 1)
+            self._run_plan(plan, lr, group["weight_decay"], self.T + 1, gi, params)
             launched.append((plan, params))
         self._pending = launched
         self._last = launched
@@ -174,30 +173,34 @@ class LearnedOptimizer(torch.optim.Optimizer):
                     self.state[p]["step"] = self.T
         return loss
 
-    def _before_apply(self, gi, plan, params, loss):
-        """Hook between plan set-up and the step (VeLO mixes weights here)."""
+    # Hook run after the feature statistics are final and before phase 2
+    # (VeLO's hypernetwork mixes the per-tensor MLPs there); None = no hook.
+    _after_stats = None
 
     # optional list collecting (phase, start_event, end_event) per step; the
     # benchmark uses it to time the dominant kernel on the launching stream
     phase_events = None
 
-    def _run_plan(self, plan, lr, weight_decay, t):
+    def _timed(self, name, fn):
         if self.phase_events is None:
-            plan.step(lr, weight_decay, t)
-            return
-        import torch
-
-        def timed(name, fn):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
             fn()
-            b.record()
-            self.phase_events.append((name, a, b))
+            return
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        self.phase_events.append((name, a, b))
 
+    def _run_plan(self, plan, lr, weight_decay, t, gi, params):
+        if self.phase_events is None and self._after_stats is None:
+            plan.step(lr, weight_decay, t)   # one C call: all phases
+            return
         plan.set_step(lr, weight_decay, t)
-        timed("factors", lambda: (plan.factor_partials(), plan.factor_finalize()))
-        timed("stats", plan.feature_stats)
-        timed("apply", plan.apply)
+        self._timed("factors", lambda: (plan.factor_partials(), plan.factor_finalize()))
+        self._timed("stats", plan.feature_stats)
+        if self._after_stats is not None:
+            self._timed("hypernet", lambda: self._after_stats(gi, plan, params))
+        self._timed("apply", plan.apply)
 
     def plans(self):
         """The StepPlans of the parameter groups (one per group)."""

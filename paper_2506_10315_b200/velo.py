@@ -1,0 +1,123 @@
+"""VeLO: the VELO_MLP per-element optimizer driven by a per-tensor LSTM
+hypernetwork that mixes a bank of per-element MLPs.
+
+The reference ships only the per-element half (the 29-column VELO_MLP feature
+set with one global MLP, features.py:24-28) and lists the hypernetwork as out
+of scope.  This module adds the build-defined hypernetwork of
+SURVEY.md section 8(a) row 15 (definition and numpy restatement:
+oracle/velo_lstm.py; device kernel: csrc/lopt_velo.cu):
+
+    per tensor and step: LSTM over [log E[f^2] (29) | tanh(t/x) (11) | loss (2)]
+    -> softmax mixing weights over K bank MLPs -> this tensor's MLP.
+
+With a bank of one MLP the mixture is that MLP, so VeLO_CUDA reduces exactly
+to the reference's VELO_MLP step (the parity anchor for the per-element path).
+PyLO's API needs the loss at every step: `optimizer.step(loss)`.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .optim import LearnedOptimizer, OptimError
+from .weights import LoptWeights, random_weights, unpack
+
+F32 = np.float32
+N_IN = 42
+
+
+class VeLOHyperNet:
+    """Hypernetwork parameters (LSTM + mixing head) and the MLP bank."""
+
+    def __init__(self, hidden: int = 16, bank_size: int = 4, seed: int = 0,
+                 hyper: np.ndarray | None = None, bank: list | None = None):
+        if not 1 <= hidden <= 64 or not 1 <= bank_size <= 16:
+            raise ValueError("hidden must be in [1, 64] and bank_size in [1, 16]")
+        self.H, self.K = hidden, bank_size
+        n = 4 * hidden * N_IN + 4 * hidden * hidden + 4 * hidden + bank_size * hidden + bank_size
+        if hyper is None:
+            rng = np.random.default_rng(seed)
+            hyper = (rng.standard_normal(n) * 0.1).astype(F32)
+            off = 4 * hidden * N_IN + 4 * hidden * hidden
+            hyper[off + hidden: off + 2 * hidden] = F32(1.0)   # forget-gate bias
+        self.hyper = np.ascontiguousarray(hyper, F32)
+        if self.hyper.size != n:
+            raise ValueError(f"hypernetwork has {self.hyper.size} parameters, expected {n}")
+        if bank is None:
+            bank = [random_weights(29, seed=seed * 1000 + k) for k in range(bank_size)]
+        if len(bank) != bank_size:
+            raise ValueError("bank size mismatch")
+        for w in bank:
+            if w.input_dim != 29:
+                raise ValueError("VeLO bank MLPs take the 29 VELO_MLP features")
+        self.bank = bank
+
+    def packed_bank(self) -> np.ndarray:
+        return np.stack([w.packed() for w in self.bank]).astype(F32)
+
+
+class _VeLOMixin:
+    """Adds the hypernetwork pass between phase 1 and phase 2."""
+
+    def _velo_init(self, hypernet: VeLOHyperNet | None):
+        self.hypernet = hypernet or VeLOHyperNet()
+        dev = self.param_groups[0]["params"][0].device
+        self._hyper_dev = torch.from_numpy(self.hypernet.hyper).to(dev)
+        self._bank_dev = torch.from_numpy(self.hypernet.packed_bank()).to(dev)
+        self._loss_dev = torch.zeros(2, dtype=torch.float32, device=dev)
+        self._loss_ema = None
+        self._lstm = {}
+
+    def _weights_for_group(self, gi, params):
+        # one weight slot per tensor, filled on the device by the hypernetwork
+        return [self.hypernet.bank[0]] * len(params), list(range(len(params)))
+
+    def _lstm_state(self, gi, params):
+        st = self._lstm.get(gi)
+        if st is None or st.shape[0] != len(params):
+            dev = params[0].device
+            st = torch.zeros(len(params), 2 * self.hypernet.H, dtype=torch.float32, device=dev)
+            self._lstm[gi] = st
+            for j, p in enumerate(params):
+                self.state[p]["lstm"] = st[j]
+        return st
+
+    def _set_loss(self, loss):
+        if loss is None:
+            raise OptimError("VeLO needs the loss: call optimizer.step(loss) (PAPER.md:600)")
+        lv = math.log(max(float(loss), 1e-8))
+        self._loss_ema = lv if self._loss_ema is None else 0.9 * self._loss_ema + 0.1 * lv
+        self._loss_dev.copy_(torch.tensor([lv, self._loss_ema], dtype=torch.float32))
+
+    def _after_stats(self, gi, plan, params):
+        st = self._lstm_state(gi, params)
+        mix = getattr(self, "_mix_out", None)
+        _lib.check(plan.L.lopt_velo_mix(
+            plan.h, self._hyper_dev.data_ptr(), st.data_ptr(), self._bank_dev.data_ptr(),
+            self._loss_dev.data_ptr(), self.hypernet.H, self.hypernet.K,
+            mix.data_ptr() if mix is not None else None,
+            torch.cuda.current_stream().cuda_stream), "velo_mix")
+
+
+class VeLO_CUDA(_VeLOMixin, LearnedOptimizer):
+    """PyLO's `VeLO_CUDA(model.parameters())` surface: VELO_MLP features, a
+    per-tensor MLP mixed by the LSTM hypernetwork, `step(loss)`."""
+
+    def __init__(self, params, lr: float = 1.0, weight_decay: float = 0.0, *,
+                 hypernet: VeLOHyperNet | None = None, **kw):
+        kw.pop("feature_set", None)
+        hn = hypernet or VeLOHyperNet()
+        super().__init__(params, lr=lr, weight_decay=weight_decay, feature_set="velo_mlp",
+                         weights=hn.bank[0], **kw)
+        self._velo_init(hn)
+
+    def step(self, closure=None, loss=None):
+        if closure is not None:
+            with torch.enable_grad():
+                loss = closure()
+        self._set_loss(loss)
+        return super().step(loss=loss)
