@@ -1,37 +1,43 @@
 // lopt_apply_tc.cu -- phase 2 of the fast path on the tensor cores.
 //
 // engine.py:657-710 fused_apply + state.py:77-90 + optim.py:171-172 for
-// 128-element tiles: features -> layer 1 (tcgen05, M=128 x N=32) -> ReLU ->
+// 128-element tiles: features -> layer 1 (tcgen05, M=128 elements) -> ReLU ->
 // layer 2 (tcgen05) -> ReLU -> layer 3 (CUDA cores, f32) -> exp -> update ->
 // decay -> store theta and the advanced accumulators.
 //
 // fp32 accuracy on the f16 tensor-core path: every operand is split in two
 // fp16 terms (x = x_hi + x_lo, relative error 2^-22) and each product is formed
-// as x_hi*W_hi + x_hi*W_lo + x_lo*W_hi with f32 accumulation.  Layer-1 inputs
+// as x_hi*W_hi + x_lo*W_hi + x_hi*W_lo with f32 accumulation.  Layer-1 inputs
 // are the normalized features (bounded by sqrt(m*n), so they fit fp16); layer-2
 // inputs are scaled by a per-tensor power of two chosen from a bound on |h1|.
 // The A operands go from registers straight into tensor memory (tcgen05.st)
 // and the MMAs read them there; only the per-tensor B operands live in smem.
 //
+// What bounds this kernel (measured with tools/probe_umma.py): an issuing
+// thread can launch one tcgen05.mma only every ~100 cycles, flat in N up to
+// 128, while the tensor pipe itself needs M*N/256 cycles.  So: few, wide MMAs
+// (layer 1 is N-packed: 4 MMAs of N=64; layer 2: 6 MMAs of N=32), and one
+// issuing warp per math warpgroup.
+//
 // Structure: persistent kernel, one CTA per SM = three 128-thread math
-// warpgroups + one MMA-issue warp.  Thread i of a warpgroup owns row i of each
-// tile (TMEM lane i).  Each warpgroup software-pipelines its contiguous tile
-// range three deep -- iteration k runs stage B of tile k-1 (layer-1 epilogue),
-// stage A of tile k (loads prefetched one iteration earlier, features) and
-// stage C of tile k-1 (layer-2 epilogue, update, stores) -- and hands operands
-// to the issue warp through mbarriers (128 arrivals each), so no math thread
-// ever waits for another; they only wait for the MMA results they consume.
+// warpgroups + three MMA-issue warps (one each).  Thread i of a warpgroup owns
+// row i of every tile (TMEM lane i).  Each warpgroup software-pipelines its
+// contiguous tile range three deep -- iteration k runs stage B of tile k-1
+// (layer-1 epilogue), stage A of tile k (features; its HBM loads were issued
+// one iteration earlier) and stage C of tile k-1 (layer-2 epilogue, update,
+// stores) -- and hands operands to its issue warp through mbarriers (128
+// arrivals), so math threads only ever wait for MMA results they consume.
 #include "lopt_fast.cuh"
 
 namespace lopt {
 
 constexpr int kWGs = 3;
 constexpr int kMathThreads = 128 * kWGs;
-constexpr int kApplyThreads = kMathThreads + 32;
-constexpr int kIssueWarp = kMathThreads / 32;
+constexpr int kApplyThreads = kMathThreads + 32 * kWGs;
+constexpr int kIssueWarp0 = kMathThreads / 32;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColsPerWG = 128;      // A1 | ACC1 | A2 | ACC2, 32 columns each
-constexpr uint32_t kOnesCol = kColsPerWG * kWGs;
+constexpr uint32_t kColsPerWG = 160;      // A1 32 | ACC1 64 | A2 32 | ACC2 32
+constexpr uint32_t kA1 = 0, kACC1 = 32, kA2 = 96, kACC2 = 128;
 
 struct __align__(128) ApplySmem {
   PrepImage img[kWGs][2];   // double-buffered per warpgroup (tensor switches)
@@ -62,7 +68,7 @@ struct TileWalker {
 };
 
 __device__ __forceinline__ void walk_to(const DevicePlan &P, TileWalker &W, int32_t t) {
-  if (W.j < 0 || t >= W.next_tile0) {
+  if (t >= W.next_tile0) {
     int j = W.j < 0 ? 0 : W.j;
     while (j + 1 < P.count && P.tensors[j + 1].tile0 <= t) j++;
     const TensorDesc *T = P.tensors + j;
@@ -77,7 +83,6 @@ __device__ __forceinline__ void walk_to(const DevicePlan &P, TileWalker &W, int3
     W.next_tile0 = j + 1 < P.count ? (int32_t)P.tensors[j + 1].tile0 : INT32_MAX;
     W.t = -2;
   }
-  const int32_t e0 = W.lo + (t - W.tile0) * kTile;
   if (t == W.t + 1 && W.n >= kTile) {
     W.b0 += kTile;
     if (W.b0 >= W.n) {
@@ -85,6 +90,7 @@ __device__ __forceinline__ void walk_to(const DevicePlan &P, TileWalker &W, int3
       W.a0++;
     }
   } else {
+    const int32_t e0 = W.lo + (t - W.tile0) * kTile;
     W.a0 = (int32_t)((uint32_t)e0 / (uint32_t)W.n);
     W.b0 = e0 - W.a0 * W.n;
   }
@@ -95,12 +101,11 @@ __device__ __forceinline__ void load_tile(const DevicePlan &P, TileWalker &W, in
                                           TileLoad &L) {
   walk_to(P, W, t);
   L.j = W.j;
-  const int32_t e = W.lo + (t - W.tile0) * kTile + row;
-  L.valid = e < W.hi;
+  const int32_t e0 = W.lo + (t - W.tile0) * kTile;
+  L.valid = e0 + row < W.hi;
   // rows past the end of the tensor compute on a valid element and are masked
   // at the store; their A rows never influence other rows
   const int r = L.valid ? row : 0;
-  const int32_t ec = L.valid ? e : W.lo + (t - W.tile0) * kTile;
   int32_t b = W.b0 + r, a = W.a0;
   if (b >= W.n) {
     if (W.n >= kTile) {
@@ -114,34 +119,26 @@ __device__ __forceinline__ void load_tile(const DevicePlan &P, TileWalker &W, in
   }
   L.a = a;
   L.b = b;
-  L.tp = const_cast<float *>(W.theta) + ec;
-  L.sp = const_cast<float4 *>(W.state) + (ec - W.lo);
+  L.tp = const_cast<float *>(W.theta) + e0 + r;
+  L.sp = const_cast<float4 *>(W.state) + (e0 + r - W.lo);
   L.w = __ldg(L.tp);
-  L.g = __ldg(W.grad + ec);
+  L.g = __ldg(W.grad + e0 + r);
   L.s = __ldg(L.sp);
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tc::smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(tc::smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
 
 __device__ __forceinline__ uint64_t f2_bits(float2 v) { return *reinterpret_cast<uint64_t *>(&v); }
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   uint64_t d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;\n" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return *reinterpret_cast<float2 *>(&d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;\n" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
   return *reinterpret_cast<float2 *>(&d);
 }
 
@@ -153,75 +150,74 @@ __device__ __forceinline__ void relu_split_f16(float a, float b, uint32_t &hi, u
   asm("cvt.rn.relu.f16x2.f32 %0, %2, %1;\n" : "=r"(lo) : "f"(a - h.x), "f"(b - h.y));
 }
 
-// The MMA-issue warp: one elected lane walks every warpgroup's event stream
-// (A1(tb), A2(tb), A1(tb+1), ..., A2(te-1)) and issues the corresponding
-// layer-1 / layer-2 MMAs when the warpgroup's 128 arrivals are in.
-__device__ void issue_loop(const DevicePlan &P, ApplySmem &S, uint32_t tbase) {
-  constexpr uint32_t kIdesc = tc::idesc_f16_f32(128, 32);
-  int64_t left[kWGs];
-  uint32_t cnt[kWGs];
-  int active = 0;
+// One issue warp per math warpgroup: lane 0 walks the warpgroup's event stream
+// A1(tb), A2(tb), A1(tb+1), ..., A2(te-1).
+__device__ void issue_loop(const DevicePlan &P, ApplySmem &S, uint32_t tbase, int g) {
+  const uint32_t idesc64 = tc::idesc_f16_f32(128, 64), idesc32 = tc::idesc_f16_f32(128, 32);
   const int64_t nwg = (int64_t)gridDim.x * kWGs;
-  for (int g = 0; g < kWGs; g++) {
-    const int64_t gwg = (int64_t)blockIdx.x * kWGs + g;
-    const int64_t tb = P.n_tiles * gwg / nwg, te = P.n_tiles * (gwg + 1) / nwg;
-    left[g] = 2 * (te - tb);
-    cnt[g] = 0;
-    active += left[g] > 0;
-  }
-  while (active > 0) {
-    bool progressed = false;
-    for (int g = 0; g < kWGs; g++) {
-      if (left[g] == 0) continue;
-      const bool is_a1 = (cnt[g] & 1u) == 0;
-      const uint32_t parity = (cnt[g] >> 1) & 1u;
-      uint64_t *bar = is_a1 ? &S.a1_ready[g] : &S.a2_ready[g];
-      if (!mbar_test(bar, parity)) continue;
-      tc::fence_after_sync();
-      const uint32_t base = tbase + kColsPerWG * g;
-      if (is_a1) {
-        const PrepImage &im = S.img[g][S.a1_buf[g]];
-        const uint32_t d = base + 32, a = base;
-        const uint64_t b0 = tc::smem_desc_kmajor(tc::smem_u32(im.b1[0]), 512, 128);
-        const uint64_t b1 = tc::smem_desc_kmajor(tc::smem_u32(im.b1[1]), 512, 128);
-        const uint64_t b2 = tc::smem_desc_kmajor(tc::smem_u32(im.b1[2]), 512, 128);
-        const uint64_t b3 = tc::smem_desc_kmajor(tc::smem_u32(im.b1[3]), 512, 128);
-        tc::mma_ts(d, a + 0, b0, kIdesc, 0);    // f_hi  * We_hi
-        tc::mma_ts(d, a + 0, b1, kIdesc, 1);    // f_hi  * We_lo
-        tc::mma_ts(d, a + 8, b0, kIdesc, 1);    // f_lo  * We_hi
-        tc::mma_ts(d, a + 16, b2, kIdesc, 1);   // bc_hi * Wbc_hi (+ bias_hi)
-        tc::mma_ts(d, a + 16, b3, kIdesc, 1);   // bc_hi * Wbc_lo (+ bias_lo)
-        tc::mma_ts(d, a + 24, b2, kIdesc, 1);   // bc_lo * Wbc_hi
-        tc::mma_commit(&S.acc1_full[g]);
-      } else {
-        const PrepImage &im = S.img[g][S.a2_buf[g]];
-        const uint32_t d = base + 96, a = base + 64;
-        uint64_t bd[5];
+  const int64_t gwg = (int64_t)blockIdx.x * kWGs + g;
+  const int32_t tb = (int32_t)(P.n_tiles * gwg / nwg), te = (int32_t)(P.n_tiles * (gwg + 1) / nwg);
+  const uint32_t base = tbase + kColsPerWG * g;
+  for (int32_t k = tb; k < te; k++) {
+    const uint32_t par = (uint32_t)((k - tb) & 1);
+    // layer 1: four N-packed MMAs
+    tc::mbar_wait(&S.a1_ready[g], par);
+    tc::fence_after_sync();
+    {
+      const PrepImage &im = S.img[g][S.a1_buf[g]];
 #pragma unroll
-        for (int q = 0; q < 5; q++) bd[q] = tc::smem_desc_kmajor(tc::smem_u32(im.b2[q]), 512, 128);
-        tc::mma_ts(d, a + 0, bd[0], kIdesc, 0);    // h_hi * W2_hi
-        tc::mma_ts(d, a + 8, bd[1], kIdesc, 1);
-        tc::mma_ts(d, a + 0, bd[2], kIdesc, 1);    // h_hi * W2_lo
-        tc::mma_ts(d, a + 8, bd[3], kIdesc, 1);
-        tc::mma_ts(d, a + 16, bd[0], kIdesc, 1);   // h_lo * W2_hi
-        tc::mma_ts(d, a + 24, bd[1], kIdesc, 1);
-        tc::mma_ts(d, tbase + kOnesCol, bd[4], kIdesc, 1);  // + b2 (hi + lo)
-        tc::mma_commit(&S.acc2_full[g]);
-      }
-      cnt[g]++;
-      if (--left[g] == 0) active--;
-      progressed = true;
+      for (int s = 0; s < 4; s++)
+        tc::mma_ts(base + kACC1, base + kA1 + 8 * s,
+                   tc::smem_desc_kmajor(tc::smem_u32(im.b1[s]), 1024, 128), idesc64, s > 0);
+      tc::mma_commit(&S.acc1_full[g]);
     }
-    if (!progressed) __nanosleep(20);
+    // layer 2: six MMAs (h_hi * W2_hi, h_hi * W2_lo, h_lo * W2_hi)
+    tc::mbar_wait(&S.a2_ready[g], par);
+    tc::fence_after_sync();
+    {
+      const PrepImage &im = S.img[g][S.a2_buf[g]];
+      uint64_t bd[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) bd[q] = tc::smem_desc_kmajor(tc::smem_u32(im.b2[q]), 512, 128);
+      const uint32_t d = base + kACC2, a = base + kA2;
+      tc::mma_ts(d, a + 0, bd[0], idesc32, 0);
+      tc::mma_ts(d, a + 8, bd[1], idesc32, 1);
+      tc::mma_ts(d, a + 0, bd[2], idesc32, 1);
+      tc::mma_ts(d, a + 8, bd[3], idesc32, 1);
+      tc::mma_ts(d, a + 16, bd[0], idesc32, 1);
+      tc::mma_ts(d, a + 24, bd[1], idesc32, 1);
+      tc::mma_commit(&S.acc2_full[g]);
+    }
   }
 }
+
+// Per-warpgroup pipeline state carried between the stages.
+struct Carry {
+  int buf = 0, j = -1;
+  bool valid = false;
+  float w = 0.0f;
+  float *theta = nullptr;
+};
+
+struct Reduce {
+  int j = -1;
+  float maxabs = 0.0f;
+  uint32_t bad = 0;
+  __device__ __forceinline__ void flush(const DevicePlan &P) {
+    if (j >= 0) {
+      if (maxabs > 0.0f)
+        atomicMax(reinterpret_cast<unsigned int *>(&P.maxabs[j]), __float_as_uint(maxabs));
+      if (bad) atomicOr(&P.status[j], LOPT_STATUS_NONFINITE_PARAM);
+    }
+  }
+};
 
 template <int KIND>
 __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   ApplySmem &S = *reinterpret_cast<ApplySmem *>(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5, wg = warp >> 2, row = tid & 127;
-  if (warp == kIssueWarp) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == kIssueWarp0) {
     tc::tmem_alloc(&S.tmem_base, kTmemCols);
     tc::tmem_relinquish();
     if ((tid & 31) == 0) {
@@ -239,24 +235,14 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
   const bool aborted = *P.abort_flag != 0;
-  if (warp < 4 && !aborted) {
-    // constant A slice for the layer-2 bias MMA: K0 = K1 = fp16 1
-    uint32_t r[16];
-#pragma unroll
-    for (int q = 0; q < 16; q++) r[q] = q == 0 ? 0x3C003C00u : 0u;
-    tc::tmem_st16(tbase + ((uint32_t)(warp * 32) << 16) + kOnesCol, r);
-    tc::tmem_st_wait();
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
 
-  if (warp == kIssueWarp) {
-    if ((tid & 31) == 0 && !aborted) issue_loop(P, S, tbase);
+  if (warp >= kIssueWarp0) {
+    if ((tid & 31) == 0 && !aborted) issue_loop(P, S, tbase, warp - kIssueWarp0);
     __syncwarp();
   } else if (!aborted) {
+    const int wg = warp >> 2, row = tid & 127;
     const uint32_t lane_addr = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t cA1 = kColsPerWG * wg, cACC1 = cA1 + 32, cA2 = cA1 + 64, cACC2 = cA1 + 96;
+    const uint32_t cbase = tbase + lane_addr + kColsPerWG * wg;
     const bool adv = P.state_advanced != 0;
     const float alpha_log2e = P.alpha * 1.4426950408889634f;
     const float beta_out = P.beta_out;
@@ -272,27 +258,19 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     if (tb < te) load_tile(P, W, tb, row, cur);
     int bufA = 1, bufA_j = -1;
     const float *rowtabA = nullptr, *coltabA = nullptr;
-    // carry from stage A(k-1) to stages B/C(k-1)
-    int prev_buf = 0, prev_j = -1;
-    bool prev_valid = false;
-    float prev_w = 0.0f;
-    float *prev_theta = nullptr;
-    // per-tensor reductions of stage C
-    int red_j = -1;
-    float maxabs = 0.0f;
-    uint32_t bad = 0;
+    Carry prev;
+    Reduce red;
 
     for (int32_t k = tb; k <= te; k++) {
       const bool hasA = k < te, hasBC = k > tb;
       const uint32_t par = (uint32_t)((k - 1 - tb) & 1);
       if (k + 1 < te) load_tile(P, W, k + 1, row, nxt);
       // ---- stage A prologue: tensor switch, table loads ------------------
-      uint4 rt0, rth, rtl, ct0, cth, ctl;
+      uint4 rt0 = make_uint4(0, 0, 0, 0), rth = rt0, rtl = rt0, ct0 = rt0, cth = rt0, ctl = rt0;
       if (hasA) {
         if (cur.j != bufA_j) {
           // every thread must be past its last read of the buffer being
-          // replaced (stage C two tiles back), then the copy must be complete
-          // before anyone reads it
+          // replaced, then the copy must be complete before anyone reads it
           bufA ^= 1;
           bufA_j = cur.j;
           const TensorDesc *T = P.tensors + cur.j;
@@ -302,39 +280,43 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
           const uint4 *src =
               reinterpret_cast<const uint4 *>(reinterpret_cast<const PrepImage *>(P.prep) + cur.j);
           uint4 *dst = reinterpret_cast<uint4 *>(&S.img[wg][bufA]);
-          for (int i = row; i < (int)(sizeof(PrepImage) / 16); i += 128) dst[i] = src[i];
+          for (int i = row; i < (int)(sizeof(PrepImage) / 16); i += 128) dst[i] = __ldg(src + i);
           tc::fence_proxy_async_smem();
           tc::bar_sync(bar_id, 128);
         }
         const uint4 *rt = reinterpret_cast<const uint4 *>(rowtabA + cur.a * kRowTab);
         const uint4 *ct = reinterpret_cast<const uint4 *>(coltabA + cur.b * kRowTab);
-        rt0 = rt[0]; rth = rt[2]; rtl = rt[3];
-        ct0 = ct[0]; cth = ct[2]; ctl = ct[3];
+        rt0 = __ldg(rt); rth = __ldg(rt + 2); rtl = __ldg(rt + 3);
+        ct0 = __ldg(ct); cth = __ldg(ct + 2); ctl = __ldg(ct + 3);
       }
       // ---- stage B (tile k-1): layer-1 epilogue -> A2 --------------------
       if (hasBC) {
         tc::mbar_wait(&S.acc1_full[wg], par);
         tc::fence_after_sync();
-        const float sdown = S.img[wg][prev_buf].s2_down;
+        const float sdown = S.img[wg][prev.buf].s2_down;
 #pragma unroll
         for (int half = 0; half < 2; half++) {
-          uint32_t h[16];
-          tc::tmem_ld16(tbase + lane_addr + cACC1 + 16 * half, h);
+          uint32_t lo[16], hi[16];
+          tc::tmem_ld16(cbase + kACC1 + 16 * half, lo);        // x_hi*W_hi + x_lo*W_hi
+          tc::tmem_ld16(cbase + kACC1 + 32 + 16 * half, hi);   // x_hi*W_lo
           tc::tmem_ld_wait();
-          if (sdown != 1.0f) {
+          uint32_t ah[8], al[8];
 #pragma unroll
-            for (int q = 0; q < 16; q++) h[q] = __float_as_uint(__uint_as_float(h[q]) * sdown);
+          for (int q = 0; q < 8; q++) {
+            float2 h = fadd2(make_float2(__uint_as_float(lo[2 * q]), __uint_as_float(lo[2 * q + 1])),
+                             make_float2(__uint_as_float(hi[2 * q]), __uint_as_float(hi[2 * q + 1])));
+            if (sdown != 1.0f) {
+              h.x *= sdown;
+              h.y *= sdown;
+            }
+            relu_split_f16(h.x, h.y, ah[q], al[q]);
           }
-          uint32_t hi8[8], lo8[8];
-#pragma unroll
-          for (int q = 0; q < 8; q++)
-            relu_split_f16(__uint_as_float(h[2 * q]), __uint_as_float(h[2 * q + 1]), hi8[q], lo8[q]);
-          tc::tmem_st8(tbase + lane_addr + cA2 + 8 * half, hi8);
-          tc::tmem_st8(tbase + lane_addr + cA2 + 16 + 8 * half, lo8);
+          tc::tmem_st8(cbase + kA2 + 8 * half, ah);
+          tc::tmem_st8(cbase + kA2 + 16 + 8 * half, al);
         }
         tc::tmem_st_wait();
         tc::fence_before_sync();
-        if (row == 0) S.a2_buf[wg] = (uint32_t)prev_buf;
+        if (row == 0) S.a2_buf[wg] = (uint32_t)prev.buf;
         mbar_arrive(&S.a2_ready[wg]);
       }
       // ---- stage A (tile k): features -> A1, advanced state --------------
@@ -353,21 +335,24 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
         // normalize (features.py:349-354) so every operand fits fp16
 #pragma unroll
         for (int q = 0; q < 16; q++) f[q] *= im.escale[q];
-        uint32_t lo16[16], hi16[16];
+        uint32_t a[16];
+        // slice s: [hi pairs of features 8s..8s+7 | lo pairs]
 #pragma unroll
-        for (int q = 0; q < 8; q++) tc::split_pair_f16(f[2 * q], f[2 * q + 1], lo16[q], lo16[8 + q]);
+        for (int s = 0; s < 2; s++)
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            tc::split_pair_f16(f[8 * s + 2 * q], f[8 * s + 2 * q + 1], a[8 * s + q], a[8 * s + 4 + q]);
+        tc::tmem_st16(cbase + kA1, a);
         uint32_t xh = 0, xl = 0;
         if (KIND == LOPT_VELO_MLP) tc::split_pair_f16(clip01(x.g) * im.escale[16], 0.0f, xh, xl);
-        hi16[0] = rth.x; hi16[1] = rth.y; hi16[2] = rth.z;
-        hi16[3] = cth.x; hi16[4] = cth.y; hi16[5] = cth.z;
-        hi16[6] = (xh & 0xFFFFu) | 0x3C000000u;   // K12 = clip_hi, K13 = fp16 1 (bias)
-        hi16[7] = 0u;
-        hi16[8] = rtl.x; hi16[9] = rtl.y; hi16[10] = rtl.z;
-        hi16[11] = ctl.x; hi16[12] = ctl.y; hi16[13] = ctl.z;
-        hi16[14] = xl & 0xFFFFu;
-        hi16[15] = 0u;
-        tc::tmem_st16(tbase + lane_addr + cA1, lo16);
-        tc::tmem_st16(tbase + lane_addr + cA1 + 16, hi16);
+        uint32_t b[16];
+        b[0] = rth.x; b[1] = rth.y; b[2] = rth.z; b[3] = cth.x;          // r5 r6 r7 rr5 rr6 rr7 c5 c6
+        b[4] = rtl.x; b[5] = rtl.y; b[6] = rtl.z; b[7] = ctl.x;
+        b[8] = cth.y; b[9] = cth.z;                                      // c7 rc5 rc6 rc7
+        b[10] = (xh & 0xFFFFu) | 0x3C000000u;                            // clip_hi, fp16 1 (bias)
+        b[11] = 0u;
+        b[12] = ctl.y; b[13] = ctl.z; b[14] = xl & 0xFFFFu; b[15] = 0u;
+        tc::tmem_st16(cbase + kA1 + 16, b);
         tc::tmem_st_wait();
         tc::fence_before_sync();
         if (row == 0) S.a1_buf[wg] = (uint32_t)bufA;
@@ -377,37 +362,30 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       if (hasBC) {
         tc::mbar_wait(&S.acc2_full[wg], par);
         tc::fence_after_sync();
-        if (prev_j != red_j) {
-          if (red_j >= 0) {
-            if (maxabs > 0.0f)
-              atomicMax(reinterpret_cast<unsigned int *>(&P.maxabs[red_j]), __float_as_uint(maxabs));
-            if (bad) atomicOr(&P.status[red_j], LOPT_STATUS_NONFINITE_PARAM);
-          }
-          red_j = prev_j;
-          maxabs = 0.0f;
-          bad = 0;
+        if (prev.j != red.j) {
+          red.flush(P);
+          red.j = prev.j;
+          red.maxabs = 0.0f;
+          red.bad = 0;
         }
-        const PrepImage &im = S.img[wg][prev_buf];
+        const PrepImage &im = S.img[wg][prev.buf];
         const float sup = im.s2_up;
         float2 d2 = make_float2(im.b3[0], 0.0f), m2 = make_float2(im.b3[1], 0.0f);
         const float4 *w30 = reinterpret_cast<const float4 *>(im.w3[0]);
         const float4 *w31 = reinterpret_cast<const float4 *>(im.w3[1]);
+        const float4 *bb2 = reinterpret_cast<const float4 *>(im.b2f);
 #pragma unroll
         for (int half = 0; half < 2; half++) {
           uint32_t h2[16];
-          tc::tmem_ld16(tbase + lane_addr + cACC2 + 16 * half, h2);
+          tc::tmem_ld16(cbase + kACC2 + 16 * half, h2);
           tc::tmem_ld_wait();
-          if (sup != 1.0f) {
-#pragma unroll
-            for (int q = 0; q < 16; q++) h2[q] = __float_as_uint(__uint_as_float(h2[q]) * sup);
-          }
 #pragma unroll
           for (int q = 0; q < 4; q++) {
-            const float4 wa = w30[4 * half + q], wb = w31[4 * half + q];
-            const float2 h01 = make_float2(fmaxf(__uint_as_float(h2[4 * q]), 0.0f),
-                                           fmaxf(__uint_as_float(h2[4 * q + 1]), 0.0f));
-            const float2 h23 = make_float2(fmaxf(__uint_as_float(h2[4 * q + 2]), 0.0f),
-                                           fmaxf(__uint_as_float(h2[4 * q + 3]), 0.0f));
+            const float4 wa = w30[4 * half + q], wb = w31[4 * half + q], bq = bb2[4 * half + q];
+            const float2 h01 = make_float2(fmaxf(fmaf(__uint_as_float(h2[4 * q]), sup, bq.x), 0.0f),
+                                           fmaxf(fmaf(__uint_as_float(h2[4 * q + 1]), sup, bq.y), 0.0f));
+            const float2 h23 = make_float2(fmaxf(fmaf(__uint_as_float(h2[4 * q + 2]), sup, bq.z), 0.0f),
+                                           fmaxf(fmaf(__uint_as_float(h2[4 * q + 3]), sup, bq.w), 0.0f));
             d2 = ffma2(h01, make_float2(wa.x, wa.y), d2);
             d2 = ffma2(h23, make_float2(wa.z, wa.w), d2);
             m2 = ffma2(h01, make_float2(wb.x, wb.y), m2);
@@ -418,33 +396,29 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
         // engine.py:537-539, exp on the SFU (fp32 tolerance path)
         const float ex = exp2f(mag * alpha_log2e);
         const float du = ds * ((dir * ex) * beta_out);
-        float out = prev_w + du;
-        if (prev_valid) {
-          maxabs = fmaxf(maxabs, fabsf(du));
-          bad |= !isfinite(out);
+        float out = prev.w + du;
+        if (prev.valid) {
+          red.maxabs = fmaxf(red.maxabs, fabsf(du));
+          red.bad |= !isfinite(out);
           if (apply_decay) out *= decay;   // optim.py:100-101
-          *prev_theta = out;
+          *prev.theta = out;
         }
       }
       // ---- shift the pipeline ---------------------------------------------
       if (hasA) {
-        prev_buf = bufA;
-        prev_j = cur.j;
-        prev_valid = cur.valid;
-        prev_w = cur.w;
-        prev_theta = cur.tp;
+        prev.buf = bufA;
+        prev.j = cur.j;
+        prev.valid = cur.valid;
+        prev.w = cur.w;
+        prev.theta = cur.tp;
         cur = nxt;
       }
     }
-    if (red_j >= 0) {
-      if (maxabs > 0.0f)
-        atomicMax(reinterpret_cast<unsigned int *>(&P.maxabs[red_j]), __float_as_uint(maxabs));
-      if (bad) atomicOr(&P.status[red_j], LOPT_STATUS_NONFINITE_PARAM);
-    }
+    red.flush(P);
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == kIssueWarp) tc::tmem_dealloc(tbase, kTmemCols);
+  if (warp == kIssueWarp0) tc::tmem_dealloc(tbase, kTmemCols);
 }
 
 static int g_num_sms = 0;

@@ -89,19 +89,25 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
     s2s[1] = ldexpf(1.0f, s2);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 32 * 16; i += blockDim.x) {
-    const int o = i >> 4, k = i & 15;
-    uint16_t hi, lo;
-    split1(w1[o * D + elem_col(KIND, k)], hi, lo);
-    img->b1[0][bslot(o, k)] = hi;
-    img->b1[1][bslot(o, k)] = lo;
+  // layer 1, N-packed (see PrepImage): slice s holds eight features q[s][0..7]
+  for (int i = threadIdx.x; i < 4 * 32 * 8; i += blockDim.x) {
+    const int s = i >> 8, o = (i >> 3) & 31, q = i & 7;
     float v = 0.0f;
-    if (k < 12) v = w1[o * D + bc_col(k)];
-    else if (k == 12) v = (KIND == LOPT_VELO_MLP) ? w1[o * D + 28] : 0.0f;
-    else if (k == 13) v = bias1[o];
+    if (s < 2) {
+      v = w1[o * D + elem_col(KIND, 8 * s + q)];
+    } else if (s == 2) {
+      v = w1[o * D + bc_col(q)];                       // r5 r6 r7 rr5 rr6 rr7 c5 c6
+    } else {
+      if (q < 4) v = w1[o * D + bc_col(8 + q)];        // c7 rc5 rc6 rc7
+      else if (q == 4) v = (KIND == LOPT_VELO_MLP) ? w1[o * D + 28] : 0.0f;   // clip
+      else if (q == 5) v = bias1[o];                   // the constant-1 column
+    }
+    uint16_t hi, lo;
     split1(v, hi, lo);
-    img->b1[2][bslot(o, k)] = hi;
-    img->b1[3][bslot(o, k)] = lo;
+    img->b1[s][bslot(o, q, 64)] = hi;            // x_hi * W_hi
+    img->b1[s][bslot(o, 8 + q, 64)] = hi;        // x_lo * W_hi
+    img->b1[s][bslot(32 + o, q, 64)] = lo;       // x_hi * W_lo
+    img->b1[s][bslot(32 + o, 8 + q, 64)] = 0;
   }
   for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
     const int o = i >> 5, k = i & 31;
@@ -110,12 +116,7 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
     img->b2[k >> 4][bslot(o, k & 15)] = hi;
     img->b2[2 + (k >> 4)][bslot(o, k & 15)] = lo;
   }
-  for (int i = threadIdx.x; i < 32 * 16; i += blockDim.x) {
-    const int o = i >> 4, k = i & 15;
-    uint16_t hi, lo;
-    split1(b2[o] * s2s[0], hi, lo);
-    img->b2[4][bslot(o, k)] = k == 0 ? hi : (k == 1 ? lo : (uint16_t)0);
-  }
+  if (threadIdx.x < 32) img->b2f[threadIdx.x] = b2[threadIdx.x];
   if (threadIdx.x < 64) img->w3[threadIdx.x >> 5][threadIdx.x & 31] = w3[threadIdx.x];
   if (threadIdx.x < 2) img->b3[threadIdx.x] = b3[threadIdx.x];
   if (threadIdx.x < 3) img->sqmr[threadIdx.x] = sqrtf(P.tscal[j].mr[threadIdx.x]);
@@ -169,33 +170,37 @@ __global__ void __launch_bounds__(kFastStatThreads) stats_fast_kernel(DevicePlan
         g4[u] = u < cnt ? __ldg(T.grad + e + u) : 0.0f;
       }
     }
-    float4 s4[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) s4[u] = u < cnt ? __ldg(T.state + (e + u - T.lo)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    // every load of the four elements is issued before any arithmetic
+    float4 s4[4], rt[4], ct[4];
     int64_t a, b;
     divmod(e, T.n, inv_n, a, b);
 #pragma unroll
     for (int u = 0; u < 4; u++) {
-      if (u > 0) {
-        b++;
-        if (b >= T.n) {
-          b = 0;
-          a++;
-        }
+      const bool ok = u < cnt;
+      s4[u] = __ldg(T.state + (ok ? e + u - T.lo : e - T.lo));
+      rt[u] = __ldg(reinterpret_cast<const float4 *>(T.rowtab + a * kRowTab));
+      ct[u] = __ldg(reinterpret_cast<const float4 *>(T.coltab + b * kRowTab));
+      if (++b >= T.n) {
+        b = 0;
+        a = a + 1 < T.m ? a + 1 : a;
       }
-      if (u >= cnt) break;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const float m = u < cnt ? 1.0f : 0.0f;   // masked lanes add zeros
       FastIn x;
       x.w = w4[u];
       advance(g4[u], s4[u], adv, P.beta, x);
-      const float4 rt = reinterpret_cast<const float4 *>(T.rowtab + a * kRowTab)[0];
-      const float4 ct = reinterpret_cast<const float4 *>(T.coltab + b * kRowTab)[0];
-      const float rc[3] = {rt.x, rt.y, rt.z}, cc[3] = {ct.x, ct.y, ct.z};
+      const float rc[3] = {rt[u].x, rt[u].y, rt[u].z}, cc[3] = {ct[u].x, ct[u].y, ct[u].z};
       float f[16];
       fast_features(x, rc, cc, sqmr, f);
 #pragma unroll
-      for (int k = 0; k < 16; k++) acc[k] = fmaf(f[k], f[k], acc[k]);
+      for (int k = 0; k < 16; k++) {
+        const float fm = f[k] * m;
+        acc[k] = fmaf(fm, fm, acc[k]);
+      }
       if (KIND == LOPT_VELO_MLP) {
-        const float cg = clip01(x.g);
+        const float cg = clip01(x.g) * m;
         acc[NE - 1] = fmaf(cg, cg, acc[NE - 1]);
       }
     }

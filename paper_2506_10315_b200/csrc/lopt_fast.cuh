@@ -18,19 +18,31 @@ constexpr int kTile = 128;
 // so W1 is used unscaled.  Layer 2 takes ReLU(h1) * 2^-s2 with s2 chosen per
 // tensor from a bound on |h1|, so it cannot overflow fp16 either (s2 = 0 for
 // every tensor of the benchmarked models).
+//
+// Layer 1 is "N-packed": each K=16 slice of A holds eight features as
+// [x_hi(8) | x_lo(8)] and its B is 64 wide, [W_hi ; W_hi] in columns 0-31 and
+// [W_lo ; 0] in columns 32-63, so ONE MMA forms x_hi*W_hi + x_lo*W_hi (cols
+// 0-31) and x_hi*W_lo (cols 32-63) for eight features; the epilogue adds the
+// two halves.  Four MMAs cover the 16 per-element features, the 12 broadcast
+// features, the VeLO clip column and the bias.  (MMA instructions, not the
+// tensor pipe, are the scarce resource at this shape: ~100 cycles of issue
+// latency per instruction per issuing thread, flat in N up to 128.)
 struct __align__(128) PrepImage {
-  uint16_t b1[4][512];      // layer 1: We_hi, We_lo, Wbc_hi(+bias_hi), Wbc_lo(+bias_lo)
-  uint16_t b2[5][512];      // layer 2: W2_hi[K0-15], W2_hi[K16-31], W2_lo x2, bias*2^-s2
+  uint16_t b1[4][1024];     // layer 1: 4 packed slices, N=64 x K=16
+  uint16_t b2[4][512];      // layer 2: W2_hi[K0-15], W2_hi[K16-31], W2_lo x2 (N=32)
+  float b2f[32];            // layer-2 bias, f32, added in the epilogue
   float w3[2][32];          // layer 3, f32
   float b3[2];
   float sqmr[3];            // sqrt(mean r_i)
   float escale[17];         // normalization scale of the per-element columns (+ clip)
   float s2_down, s2_up;     // 2^-s2, 2^s2
+  float pad[8];
 };
 static_assert(sizeof(PrepImage) % 16 == 0, "PrepImage must be 16-byte granular");
 
-__device__ __forceinline__ int bslot(int o, int k) {
-  return ((k >> 3) * 512 + (o >> 3) * 128 + (o & 7) * 16 + (k & 7) * 2) >> 1;
+// canonical K-major no-swizzle index of (row o, k) in an N-row, K=16 slice
+__device__ __forceinline__ int bslot(int o, int k, int N = 32) {
+  return ((k >> 3) * (N * 16) + (o >> 3) * 128 + (o & 7) * 16 + (k & 7) * 2) >> 1;
 }
 
 // Element-wise column order of the A operand (reference column indices):

@@ -1,6 +1,6 @@
-"""Latency/throughput probe of tcgen05.mma kind::f16 at M=128 (one CTA, one
-issuing thread): SM cycles per commit round trip for batch sizes, N, and the
-A operand in tensor memory vs shared memory."""
+"""Latency/throughput probe of tcgen05.mma kind::f16 at M=128 (one CTA):
+SM cycles per commit round trip for batch sizes and N, A in tensor memory vs
+shared memory, and with 1-4 warps issuing independent MMA streams."""
 import os
 import sys
 
@@ -10,7 +10,7 @@ import torch
 from paper_2506_10315_b200 import _lib
 
 L = _lib.require_cuda()
-out = torch.zeros(1, dtype=torch.int64, device="cuda")
+out = torch.zeros(4, dtype=torch.int64, device="cuda")
 s = torch.cuda.current_stream().cuda_stream
 for a_smem in (0, 1):
     for N in (32, 64, 128, 256):
@@ -18,6 +18,18 @@ for a_smem in (0, 1):
             flags = batch | (N << 16) | (a_smem << 28)
             _lib.check(L.lopt_probe_umma(flags, 1000, out.data_ptr(), s))
             torch.cuda.synchronize()
-            c = int(out.item())
+            c = int(out[0].item())
             print(f"A={'smem' if a_smem else 'tmem'} N={N:3d} batch={batch:3d}: "
                   f"{c:6d} cycles/round {c / batch:7.1f} cycles/MMA")
+for issuers in (1, 2, 3, 4):
+    for batch in (8, 64):
+        out.zero_()
+        flags = batch | (issuers << 12) | (64 << 16)
+        if issuers == 1:
+            flags |= 0  # single-issuer path of the probe (N=64)
+        _lib.check(L.lopt_probe_umma(flags, 500, out.data_ptr(), s))
+        torch.cuda.synchronize()
+        c = [int(v) for v in out.tolist()[:issuers]]
+        mx = max(c)
+        print(f"issuers={issuers} N=64 batch={batch:3d}: max {mx} cycles/round per issuer, "
+              f"aggregate {mx / (batch * issuers):6.1f} cycles/MMA")
