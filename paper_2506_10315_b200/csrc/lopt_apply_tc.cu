@@ -6,208 +6,380 @@
 // decay -> store theta and the advanced accumulators.
 //
 // fp32 accuracy on the f16 tensor-core path: every operand is split in two
-// fp16 terms (x = x_hi + x_lo, relative error 2^-22) and each product is formed
-// as x_hi*W_hi + x_lo*W_hi + x_hi*W_lo with f32 accumulation.  Layer-1 inputs
-// are the normalized features (bounded by sqrt(m*n), so they fit fp16); layer-2
-// inputs are scaled by a per-tensor power of two chosen from a bound on |h1|.
-// The A operands go from registers straight into tensor memory (tcgen05.st)
-// and the MMAs read them there; only the per-tensor B operands live in smem.
+// fp16 terms and each product is x_hi*W_hi + x_lo*W_hi + x_hi*W_lo with f32
+// accumulation (see PrepImage in lopt_fast.cuh for the operand layout).
 //
-// What bounds this kernel (measured with tools/probe_umma.py): an issuing
-// thread can launch one tcgen05.mma only every ~100 cycles, flat in N up to
-// 128, while the tensor pipe itself needs M*N/256 cycles.  So: few, wide MMAs
-// (layer 1 is N-packed: 4 MMAs of N=64; layer 2: 6 MMAs of N=32), and one
-// issuing warp per math warpgroup.
+// Structure: a warp-specialized persistent kernel, one CTA per SM, that
+// streams the CTA's contiguous range of tiles through a pipeline:
 //
-// Structure: persistent kernel, one CTA per SM = three 128-thread math
-// warpgroups + three MMA-issue warps (one each).  Thread i of a warpgroup owns
-// row i of every tile (TMEM lane i).  Each warpgroup software-pipelines its
-// contiguous tile range three deep -- iteration k runs stage B of tile k-1
-// (layer-1 epilogue), stage A of tile k (features; its HBM loads were issued
-// one iteration earlier) and stage C of tile k-1 (layer-2 epilogue, update,
-// stores) -- and hands operands to its issue warp through mbarriers (128
-// arrivals), so math threads only ever wait for MMA results they consume.
+//   producer warp  --TMA bulk copies-->  smem ring of kRing tile slots
+//                  (theta, g, {M1,M2,M3,V} quads, row-table entry, and the
+//                   tensor's operand image when the tensor changes)
+//   WG_A (128 thr) features -> E/B operands in TMEM slot   --op_ready-->
+//   MMA warp L1    6 x tcgen05.mma -> acc                  --acc1_full-->
+//   WG_B (128 thr) ReLU + fp16 split of h1 -> H operand    --h_ready-->
+//   MMA warp L2    7 x tcgen05.mma -> acc                  --acc2_full-->
+//   WG_C (128 thr) ReLU, layer 3, exp, update, store theta --slot_free/data_free-->
+//
+// Thread i of each warpgroup owns TMEM lane i = lane i of every tile.  TMEM
+// holds kSlots tiles in flight (64 columns each: operands, accumulator), so
+// MMA latency is hidden by the other tiles' CUDA-core work instead of being
+// waited out.  All hand-offs are mbarriers; MMAs are issued by one elected
+// lane of a converged warp (descriptors in uniform registers, back-to-back
+// issue).
+//
+// Tiles of tensors with n % 128 == 0 are (row, 128-column block) pairs in
+// column-block-major order, so consecutive tiles share their column-table
+// entries (kept in WG_A's registers); other tensors use flat 128-element tiles.
+#include <cstdio>
+#include <cstdlib>
+
 #include "lopt_fast.cuh"
 
 namespace lopt {
 
-constexpr int kWGs = 3;
-constexpr int kMathThreads = 128 * kWGs;
-constexpr int kApplyThreads = kMathThreads + 32 * kWGs;
-constexpr int kIssueWarp0 = kMathThreads / 32;
+constexpr int kRing = 16;      // smem tile slots (prefetch + in flight)
+constexpr int kSlots = 7;      // TMEM tile slots
+constexpr int kImgs = 4;       // smem operand images (tensor switches in flight)
+constexpr int kRoleWGs = 2;    // warpgroups per role (even / odd tiles)
+constexpr int kApplyThreads = 3 * kRoleWGs * 128 + (kRoleWGs + 2) * 32;
+constexpr int kWarpA = 0, kWarpB = 4 * kRoleWGs, kWarpC = 8 * kRoleWGs;
+constexpr int kWarpProducer = 12 * kRoleWGs;   // kRoleWGs producer warps (even / odd tiles)
+constexpr int kWarpMma1 = kWarpProducer + kRoleWGs, kWarpMma2 = kWarpMma1 + 1;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColsPerWG = 160;      // A1 32 | ACC1 64 | A2 32 | ACC2 32
-constexpr uint32_t kA1 = 0, kACC1 = 32, kA2 = 96, kACC2 = 128;
+constexpr uint32_t kOneCol = 64 * kSlots;   // shared constant slice
+static_assert(kOneCol + 8 <= kTmemCols, "TMEM budget");
 
-struct __align__(128) ApplySmem {
-  PrepImage img[kWGs][2];   // double-buffered per warpgroup (tensor switches)
-  uint64_t a1_ready[kWGs], a2_ready[kWGs];     // 128 arrivals: operands in TMEM
-  uint64_t acc1_full[kWGs], acc2_full[kWGs];   // tcgen05.commit: results in TMEM
-  uint32_t a1_buf[kWGs], a2_buf[kWGs];         // PrepImage buffer of the pending MMA
+constexpr int32_t kFlagRowblock = 1, kFlagSlow = 2;
+
+// Written by the producer for every tile it stages.  Lane pointers are
+// pre-offset to the tile's first element, so lane i uses ptr + i.
+struct __align__(16) TileMeta {
+  int32_t j;        // tensor
+  int32_t flags;    // kFlagRowblock | kFlagSlow (lanes read theta/g/state from global)
+  int32_t v0, v1;   // valid lanes [v0, v1)
+  int32_t img;      // operand image buffer
+  int32_t img_par;  // parity of that buffer's current load (img_full phase)
+  int32_t b0;       // rowblock: first column of the tile (column-entry cache key)
+  int32_t e0, n;    // flat: element of lane 0, columns (table indices)
+  int32_t pad0[3];
+  float *theta;     // &theta[e0]
+  const float *grad;// &grad[e0]
+  float4 *state;    // &state[e0 - lo]
+  const float *rowtab, *coltab;
+  void *pad;
+};
+
+struct __align__(128) Stage {
+  float4 st[128];       // {M1, M2, M3, V}
+  float th[128];
+  float gr[128];
+  uint4 rowent[4];      // rowblock: the tile row's table entry
+  TileMeta meta;
+};
+
+struct __align__(1024) ApplySmem {
+  PrepImage img[kImgs];
+  Stage stage[kRing];
+  uint64_t full[kRing];        // producer -> A, B, C: tile staged (TMA complete_tx)
+  uint64_t data_free[kRing];   // C -> producer (128 arrivals)
+  uint64_t op_ready[kSlots];   // A -> MMA1 (128)
+  uint64_t acc1_full[kSlots];  // MMA1 -> B (commit)
+  uint64_t h_ready[kSlots];    // B -> MMA2 (128)
+  uint64_t acc2_full[kSlots];  // MMA2 -> C (commit)
+  uint64_t slot_free[kSlots];  // C -> A (one arrival per warp)
+  uint64_t img_full[kImgs];    // producer -> A: operand image loaded (TMA complete_tx)
+  int32_t c_done[kRoleWGs][4]; // C warps: last tile finished (image-buffer reuse)
   uint32_t tmem_base;
 };
-
-struct TileLoad {
-  int j;
-  bool valid;
-  int32_t a, b;      // (row, column) of the element (clamped into the tensor)
-  float *tp;         // &theta[e]
-  float4 *sp;        // &state[e - lo]
-  float w, g;
-  float4 s;
-};
-
-// Walks a warpgroup's contiguous tile range: current tensor, tile origin
-// (row a0, column b0) advanced incrementally from tile to tile.
-// (32-bit indices: fast-mode plans require < 2^31 elements per tensor and tiles)
-struct TileWalker {
-  int j = -1;
-  int32_t next_tile0 = -1, tile0 = 0, lo = 0, hi = 0, n = 1, t = -2, a0 = 0, b0 = 0;
-  const float *theta = nullptr, *grad = nullptr;
-  const float4 *state = nullptr;
-};
-
-__device__ __forceinline__ void walk_to(const DevicePlan &P, TileWalker &W, int32_t t) {
-  if (t >= W.next_tile0) {
-    int j = W.j < 0 ? 0 : W.j;
-    while (j + 1 < P.count && P.tensors[j + 1].tile0 <= t) j++;
-    const TensorDesc *T = P.tensors + j;
-    W.j = j;
-    W.tile0 = (int32_t)T->tile0;
-    W.lo = (int32_t)T->lo;
-    W.hi = (int32_t)T->hi;
-    W.n = (int32_t)T->n;
-    W.theta = T->theta;
-    W.grad = T->grad;
-    W.state = T->state;
-    W.next_tile0 = j + 1 < P.count ? (int32_t)P.tensors[j + 1].tile0 : INT32_MAX;
-    W.t = -2;
-  }
-  if (t == W.t + 1 && W.n >= kTile) {
-    W.b0 += kTile;
-    if (W.b0 >= W.n) {
-      W.b0 -= W.n;
-      W.a0++;
-    }
-  } else {
-    const int32_t e0 = W.lo + (t - W.tile0) * kTile;
-    W.a0 = (int32_t)((uint32_t)e0 / (uint32_t)W.n);
-    W.b0 = e0 - W.a0 * W.n;
-  }
-  W.t = t;
-}
-
-__device__ __forceinline__ void load_tile(const DevicePlan &P, TileWalker &W, int32_t t, int row,
-                                          TileLoad &L) {
-  walk_to(P, W, t);
-  L.j = W.j;
-  const int32_t e0 = W.lo + (t - W.tile0) * kTile;
-  L.valid = e0 + row < W.hi;
-  // rows past the end of the tensor compute on a valid element and are masked
-  // at the store; their A rows never influence other rows
-  const int r = L.valid ? row : 0;
-  int32_t b = W.b0 + r, a = W.a0;
-  if (b >= W.n) {
-    if (W.n >= kTile) {
-      b -= W.n;
-      a++;
-    } else {
-      const uint32_t q = (uint32_t)b / (uint32_t)W.n;
-      a += (int32_t)q;
-      b -= (int32_t)q * W.n;
-    }
-  }
-  L.a = a;
-  L.b = b;
-  L.tp = const_cast<float *>(W.theta) + e0 + r;
-  L.sp = const_cast<float4 *>(W.state) + (e0 + r - W.lo);
-  L.w = __ldg(L.tp);
-  L.g = __ldg(W.grad + e0 + r);
-  L.s = __ldg(L.sp);
-}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tc::smem_u32(bar)) : "memory");
 }
+// One arrival per warp (the barriers count warps, not threads): the lanes'
+// prior writes are ordered before the elected lane's release by __syncwarp.
+__device__ __forceinline__ void warp_arrive(uint64_t *bar) {
+  __syncwarp();
+  if (tc::elect_one()) mbar_arrive(bar);
+  __syncwarp();
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tc::smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+// global -> shared bulk copy (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+      : "memory");
+}
 
 __device__ __forceinline__ uint64_t f2_bits(float2 v) { return *reinterpret_cast<uint64_t *>(&v); }
+__device__ __forceinline__ float2 bits_f2(uint64_t v) { return *reinterpret_cast<float2 *>(&v); }
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   uint64_t d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;\n" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
-  return *reinterpret_cast<float2 *>(&d);
+  return bits_f2(d);
 }
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;\n" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
-  return *reinterpret_cast<float2 *>(&d);
+  asm("mul.rn.f32x2 %0, %1, %2;\n" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return bits_f2(d);
 }
 
-// ReLU fused into a two-term fp16 split: hi truncates toward zero (so the
-// residual of a positive value is non-negative), both conversions clamp at 0.
-__device__ __forceinline__ void relu_split_f16(float a, float b, uint32_t &hi, uint32_t &lo) {
-  asm("cvt.rz.relu.f16x2.f32 %0, %2, %1;\n" : "=r"(hi) : "f"(a), "f"(b));
-  const float2 h = tc::unpack_f16x2(hi);
-  asm("cvt.rn.relu.f16x2.f32 %0, %2, %1;\n" : "=r"(lo) : "f"(a - h.x), "f"(b - h.y));
+// Two-term fp16 split of a pair, x = hi + lo: hi rounds to nearest, the
+// residual x - hi is formed exactly by a mixed f32 - f16 subtract (FHADD), so
+// a pair costs four instructions (no f16 -> f32 unpack).
+__device__ __forceinline__ void split2(float a, float b, uint32_t &hi, uint32_t &lo) {
+  asm("{\n"
+      ".reg .b16 h0, h1, n0, n1;\n"
+      ".reg .f32 r0, r1;\n"
+      "cvt.rn.f16x2.f32 %0, %3, %2;\n"
+      "mov.b32 {h0, h1}, %0;\n"
+      "neg.f16 n0, h0;\n"
+      "neg.f16 n1, h1;\n"
+      "add.rn.f32.f16 r0, n0, %2;\n"
+      "add.rn.f32.f16 r1, n1, %3;\n"
+      "cvt.rn.f16x2.f32 %1, r1, r0;\n"
+      "}\n"
+      : "=r"(hi), "=r"(lo)
+      : "f"(a), "f"(b));
+}
+// ReLU fused into the split: hi truncates toward zero (so the residual of a
+// positive value is non-negative) and both conversions clamp at 0.
+__device__ __forceinline__ void relu_split2(float a, float b, uint32_t &hi, uint32_t &lo) {
+  asm("{\n"
+      ".reg .b16 h0, h1, n0, n1;\n"
+      ".reg .f32 r0, r1;\n"
+      "cvt.rz.relu.f16x2.f32 %0, %3, %2;\n"
+      "mov.b32 {h0, h1}, %0;\n"
+      "neg.f16 n0, h0;\n"
+      "neg.f16 n1, h1;\n"
+      "add.rn.f32.f16 r0, n0, %2;\n"
+      "add.rn.f32.f16 r1, n1, %3;\n"
+      "cvt.rn.relu.f16x2.f32 %1, r1, r0;\n"
+      "}\n"
+      : "=r"(hi), "=r"(lo)
+      : "f"(a), "f"(b));
 }
 
-// One issue warp per math warpgroup: lane 0 walks the warpgroup's event stream
-// A1(tb), A2(tb), A1(tb+1), ..., A2(te-1).
-__device__ void issue_loop(const DevicePlan &P, ApplySmem &S, uint32_t tbase, int g) {
-  const uint32_t idesc64 = tc::idesc_f16_f32(128, 64), idesc32 = tc::idesc_f16_f32(128, 32);
-  const int64_t nwg = (int64_t)gridDim.x * kWGs;
-  const int64_t gwg = (int64_t)blockIdx.x * kWGs + g;
-  const int32_t tb = (int32_t)(P.n_tiles * gwg / nwg), te = (int32_t)(P.n_tiles * (gwg + 1) / nwg);
-  const uint32_t base = tbase + kColsPerWG * g;
-  for (int32_t k = tb; k < te; k++) {
-    const uint32_t par = (uint32_t)((k - tb) & 1);
-    // layer 1: four N-packed MMAs
-    tc::mbar_wait(&S.a1_ready[g], par);
-    tc::fence_after_sync();
-    {
-      const PrepImage &im = S.img[g][S.a1_buf[g]];
-#pragma unroll
-      for (int s = 0; s < 4; s++)
-        tc::mma_ts(base + kACC1, base + kA1 + 8 * s,
-                   tc::smem_desc_kmajor(tc::smem_u32(im.b1[s]), 1024, 128), idesc64, s > 0);
-      tc::mma_commit(&S.acc1_full[g]);
+// The producer (one lane): walks the CTA's tiles in order and stages each one
+// with bulk copies (theta, g, the state quads of the valid lanes, the row's
+// table entry for row-block tiles, the tensor's operand image on a switch).
+struct Producer {
+  int j = -1;
+  int32_t left = 0;               // tiles of tensor j still to stage
+  int32_t a = 0, b0 = 0, e0 = 0;  // rowblock: row, first column; flat: first element
+  int32_t n = 1, lo = 0, hi = 0, a_lo = 0, a_end = 0;
+  bool rb = false, aligned = false;
+  float *theta = nullptr;
+  const float *grad = nullptr, *rowtab = nullptr, *coltab = nullptr;
+  float4 *state = nullptr;
+
+  __device__ __forceinline__ void load_tensor(const DevicePlan &P, int jj, int32_t q) {
+    const TensorDesc *T = P.tensors + jj;
+    j = jj;
+    n = (int32_t)T->n;
+    lo = (int32_t)T->lo;
+    hi = (int32_t)T->hi;
+    rb = T->rowblock != 0;
+    a_lo = T->a_lo;
+    a_end = T->a_lo + T->m_rows;
+    theta = T->theta;
+    grad = T->grad;
+    state = T->state;
+    rowtab = T->rowtab;
+    coltab = T->coltab;
+    aligned = ((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+    left = T->tiles - q;
+    if (rb) {
+      const int32_t mr = T->m_rows;
+      a = a_lo + q % mr;
+      b0 = (q / mr) * kTile;
+    } else {
+      e0 = lo + q * kTile;
     }
-    // layer 2: six MMAs (h_hi * W2_hi, h_hi * W2_lo, h_lo * W2_hi)
-    tc::mbar_wait(&S.a2_ready[g], par);
-    tc::fence_after_sync();
-    {
-      const PrepImage &im = S.img[g][S.a2_buf[g]];
-      uint64_t bd[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) bd[q] = tc::smem_desc_kmajor(tc::smem_u32(im.b2[q]), 512, 128);
-      const uint32_t d = base + kACC2, a = base + kA2;
-      tc::mma_ts(d, a + 0, bd[0], idesc32, 0);
-      tc::mma_ts(d, a + 8, bd[1], idesc32, 1);
-      tc::mma_ts(d, a + 0, bd[2], idesc32, 1);
-      tc::mma_ts(d, a + 8, bd[3], idesc32, 1);
-      tc::mma_ts(d, a + 16, bd[0], idesc32, 1);
-      tc::mma_ts(d, a + 24, bd[1], idesc32, 1);
-      tc::mma_commit(&S.acc2_full[g]);
+  }
+
+  __device__ __forceinline__ void seek(const DevicePlan &P, int32_t t) {
+    int jj = 0;
+    while (jj + 1 < P.count && P.tensors[jj + 1].tile0 <= t) jj++;
+    while (P.tensors[jj].tiles == 0 && jj + 1 < P.count) jj++;
+    load_tensor(P, jj, t - (int32_t)P.tensors[jj].tile0);
+  }
+
+  __device__ __forceinline__ void advance(const DevicePlan &P) {
+    if (--left == 0) {
+      int jj = j + 1;
+      while (jj < P.count && P.tensors[jj].tiles == 0) jj++;
+      if (jj < P.count) load_tensor(P, jj, 0);
+      return;
+    }
+    if (rb) {
+      if (++a == a_end) {
+        a = a_lo;
+        b0 += kTile;
+      }
+    } else {
+      e0 += kTile;
+    }
+  }
+
+  __device__ __forceinline__ void stage(Stage &st, uint64_t *full, int img, int img_par,
+                                        int dbg = 0) {
+    TileMeta mt;
+    mt.j = j;
+    mt.b0 = b0;
+    const int32_t el0 = rb ? a * n + b0 : e0;
+    mt.e0 = el0;
+    mt.n = n;
+    int32_t v0 = max(0, lo - el0), v1 = min(kTile, hi - el0);
+    if (v1 <= v0) v0 = v1 = 0;
+    mt.v0 = v0;
+    mt.v1 = v1;
+    const bool fast = aligned && ((el0 + v0) & 3) == 0 && ((v1 - v0) & 3) == 0;
+    mt.flags = (rb ? kFlagRowblock : 0) | (fast ? 0 : kFlagSlow);
+    mt.img = img;
+    mt.img_par = img_par;
+    mt.pad0[0] = mt.pad0[1] = mt.pad0[2] = 0;
+    mt.theta = theta + el0;
+    mt.grad = grad + el0;
+    mt.state = state + (el0 - lo);
+    mt.rowtab = rowtab;
+    mt.coltab = coltab;
+    mt.pad = nullptr;
+    st.meta = mt;
+    const uint32_t nv = (uint32_t)(v1 - v0);
+    const uint32_t bytes = (fast ? 24u * nv : 0u) + (rb ? 64u : 0u);
+    if (dbg & 16) {
+      mbar_arrive(full);
+      return;
+    }
+    mbar_arrive_tx(full, bytes);
+    if (fast && nv > 0) {
+      bulk_g2s(&st.th[v0], theta + el0 + v0, 4 * nv, full);
+      bulk_g2s(&st.gr[v0], grad + el0 + v0, 4 * nv, full);
+      bulk_g2s(&st.st[v0], state + (el0 + v0 - lo), 16 * nv, full);
+    }
+    if (rb) bulk_g2s(st.rowent, rowtab + (int64_t)a * kRowTab, 64, full);
+  }
+};
+
+// x5 x6 x7 and the scaled fp16 hi/lo operand words of a row/column table entry
+struct Entry {
+  float x[3];
+  uint32_t hi[3], lo[3];
+};
+__device__ __forceinline__ void load_entry(const float *tab, int32_t i, Entry &E) {
+  const uint4 *p = reinterpret_cast<const uint4 *>(tab + (int64_t)i * kRowTab);
+  const uint4 v = __ldg(p), h = __ldg(p + 2), l = __ldg(p + 3);
+  E.x[0] = __uint_as_float(v.x); E.x[1] = __uint_as_float(v.y); E.x[2] = __uint_as_float(v.z);
+  E.hi[0] = h.x; E.hi[1] = h.y; E.hi[2] = h.z;
+  E.lo[0] = l.x; E.lo[1] = l.y; E.lo[2] = l.z;
+}
+
+__device__ __forceinline__ void issue_layer1(const PrepImage &im, uint32_t op, uint32_t acc, uint64_t *bar) {
+  const uint32_t idesc = tc::idesc_f16_f32(128, 32);
+  const uint64_t w_eh = tc::smem_desc_kmajor(tc::smem_u32(im.b1[0]), 512, 128);
+  const uint64_t w_el = tc::smem_desc_kmajor(tc::smem_u32(im.b1[1]), 512, 128);
+  const uint64_t w_bh = tc::smem_desc_kmajor(tc::smem_u32(im.b1[2]), 512, 128);
+  const uint64_t w_bl = tc::smem_desc_kmajor(tc::smem_u32(im.b1[3]), 512, 128);
+  const uint32_t d = acc;
+  tc::mma_ts(d, op + 0, w_eh, idesc, 0);
+  tc::mma_ts(d, op + 8, w_eh, idesc, 1);
+  tc::mma_ts(d, op + 0, w_el, idesc, 1);
+  tc::mma_ts(d, op + 16, w_bh, idesc, 1);
+  tc::mma_ts(d, op + 24, w_bh, idesc, 1);
+  tc::mma_ts(d, op + 16, w_bl, idesc, 1);
+  tc::mma_commit(bar);
+}
+
+__device__ __forceinline__ void issue_layer2(const PrepImage &im, uint32_t op, uint32_t acc,
+                                             uint32_t one, uint64_t *bar) {
+  const uint32_t idesc = tc::idesc_f16_f32(128, 32);
+  const uint64_t h0 = tc::smem_desc_kmajor(tc::smem_u32(im.b2[0]), 512, 128);
+  const uint64_t h1 = tc::smem_desc_kmajor(tc::smem_u32(im.b2[1]), 512, 128);
+  const uint64_t l0 = tc::smem_desc_kmajor(tc::smem_u32(im.b2[2]), 512, 128);
+  const uint64_t l1 = tc::smem_desc_kmajor(tc::smem_u32(im.b2[3]), 512, 128);
+  const uint64_t bb = tc::smem_desc_kmajor(tc::smem_u32(im.b2[4]), 512, 128);
+  const uint32_t d = acc;
+  tc::mma_ts(d, op + 0, h0, idesc, 0);
+  tc::mma_ts(d, op + 8, h1, idesc, 1);
+  tc::mma_ts(d, op + 16, h0, idesc, 1);
+  tc::mma_ts(d, op + 24, h1, idesc, 1);
+  tc::mma_ts(d, op + 0, l0, idesc, 1);
+  tc::mma_ts(d, op + 8, l1, idesc, 1);
+  tc::mma_ts(d, one, bb, idesc, 1);
+  tc::mma_commit(bar);
+}
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+// max that propagates NaN (any non-finite update poisons the tensor's flag)
+__device__ __forceinline__ float max_nan_abs(float m, float x) {
+  float y;
+  asm("max.NaN.f32 %0, %1, %2;\n" : "=f"(y) : "f"(m), "f"(fabsf(x)));
+  return y;
+}
+
+// Timing trace (LOPT_APPLY_DEBUG & 32): CTA 0 records clock64 at the pipeline
+// hand-offs of its first kTraceTiles tiles.
+constexpr int kTraceTiles = 64;
+__device__ long long g_trace[kTraceTiles][8];
+__device__ __forceinline__ void trace(const DevicePlan &P, int32_t i, int ev) {
+  if ((P.dbg & 32) && blockIdx.x == 0 && i < kTraceTiles && (threadIdx.x & 31) == 0)
+    g_trace[i][ev] = clock64();
+}
+
+// Ring position of a role: slot index and phase parity, advanced per tile.
+template <int N>
+struct Cursor {
+  int i = 0;
+  uint32_t phase = 0;
+  bool wrapped = false;
+  __device__ __forceinline__ void next() {
+    if (++i == N) {
+      i = 0;
+      phase ^= 1u;
+      wrapped = true;
+    }
+  }
+};
+
+#ifdef LOPT_WATCHDOG
+__device__ __forceinline__ void wd_wait(uint64_t *bar, uint32_t parity, int tag, int32_t i) {
+  long long n = 0;
+  while (!tc::mbar_try(bar, parity)) {
+    if (++n == (1ll << 24) && blockIdx.x < 3 && (threadIdx.x & 31) == 0) {
+      printf("apply hang: block %d warp %d tag %d tile %d parity %u\n", blockIdx.x,
+             threadIdx.x >> 5, tag, i, parity);
     }
   }
 }
+#define WAIT(bar, par, tag) wd_wait(bar, par, tag, i)
+#else
+#define WAIT(bar, par, tag) tc::mbar_wait(bar, par)
+#endif
 
-// Per-warpgroup pipeline state carried between the stages.
-struct Carry {
-  int buf = 0, j = -1;
-  bool valid = false;
-  float w = 0.0f;
-  float *theta = nullptr;
-};
-
-struct Reduce {
-  int j = -1;
-  float maxabs = 0.0f;
-  uint32_t bad = 0;
-  __device__ __forceinline__ void flush(const DevicePlan &P) {
-    if (j >= 0) {
-      if (maxabs > 0.0f)
-        atomicMax(reinterpret_cast<unsigned int *>(&P.maxabs[j]), __float_as_uint(maxabs));
-      if (bad) atomicOr(&P.status[j], LOPT_STATUS_NONFINITE_PARAM);
+// Ring position of a role that takes every kRoleWGs-th tile.
+template <int N>
+struct Stride {
+  int i;
+  uint32_t phase = 0;
+  bool wrapped = false;
+  __device__ __forceinline__ explicit Stride(int start) : i(start) {}
+  __device__ __forceinline__ void next() {
+    i += kRoleWGs;
+    if (i >= N) {
+      i -= N;
+      phase ^= 1u;
+      wrapped = true;
     }
   }
 };
@@ -216,224 +388,370 @@ template <int KIND>
 __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   ApplySmem &S = *reinterpret_cast<ApplySmem *>(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5;
-  if (warp == kIssueWarp0) {
+  const int tid = threadIdx.x;
+  // warp-uniform role index the compiler can prove uniform
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int row = tid & 127;
+  if (warp == 0) {
     tc::tmem_alloc(&S.tmem_base, kTmemCols);
     tc::tmem_relinquish();
-    if ((tid & 31) == 0) {
-      for (int g = 0; g < kWGs; g++) {
-        tc::mbar_init(&S.a1_ready[g], 128);
-        tc::mbar_init(&S.a2_ready[g], 128);
-        tc::mbar_init(&S.acc1_full[g], 1);
-        tc::mbar_init(&S.acc2_full[g], 1);
-      }
-      tc::mbar_fence_init();
+  }
+  if (tid == 0) {
+    for (int r = 0; r < kRing; r++) {
+      tc::mbar_init(&S.full[r], 1);
+      tc::mbar_init(&S.data_free[r], 4);
     }
+    for (int b = 0; b < kImgs; b++) tc::mbar_init(&S.img_full[b], 1);
+    for (int w = 0; w < kRoleWGs; w++)
+      for (int q = 0; q < 4; q++) S.c_done[w][q] = -1;
+    for (int s = 0; s < kSlots; s++) {
+      tc::mbar_init(&S.op_ready[s], 4);
+      tc::mbar_init(&S.acc1_full[s], 1);
+      tc::mbar_init(&S.h_ready[s], 4);
+      tc::mbar_init(&S.acc2_full[s], 1);
+      tc::mbar_init(&S.slot_free[s], 4);
+    }
+    tc::mbar_fence_init();
   }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = S.tmem_base;
-  const bool aborted = *P.abort_flag != 0;
-
-  if (warp >= kIssueWarp0) {
-    if ((tid & 31) == 0 && !aborted) issue_loop(P, S, tbase, warp - kIssueWarp0);
-    __syncwarp();
-  } else if (!aborted) {
-    const int wg = warp >> 2, row = tid & 127;
-    const uint32_t lane_addr = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t cbase = tbase + lane_addr + kColsPerWG * wg;
-    const bool adv = P.state_advanced != 0;
-    const float alpha_log2e = P.alpha * 1.4426950408889634f;
-    const float beta_out = P.beta_out;
-    const float ds = P.step->ds, decay = P.step->decay;
-    const bool apply_decay = P.step->apply_decay != 0;
-    const int bar_id = 1 + wg;
-    const int64_t nwg = (int64_t)gridDim.x * kWGs;
-    const int64_t gwg = (int64_t)blockIdx.x * kWGs + wg;
-    const int32_t tb = (int32_t)(P.n_tiles * gwg / nwg), te = (int32_t)(P.n_tiles * (gwg + 1) / nwg);
-
-    TileWalker W;
-    TileLoad cur, nxt;
-    if (tb < te) load_tile(P, W, tb, row, cur);
-    int bufA = 1, bufA_j = -1;
-    const float *rowtabA = nullptr, *coltabA = nullptr;
-    Carry prev;
-    Reduce red;
-
-    for (int32_t k = tb; k <= te; k++) {
-      const bool hasA = k < te, hasBC = k > tb;
-      const uint32_t par = (uint32_t)((k - 1 - tb) & 1);
-      if (k + 1 < te) load_tile(P, W, k + 1, row, nxt);
-      // ---- stage A prologue: tensor switch, table loads ------------------
-      uint4 rt0 = make_uint4(0, 0, 0, 0), rth = rt0, rtl = rt0, ct0 = rt0, cth = rt0, ctl = rt0;
-      if (hasA) {
-        if (cur.j != bufA_j) {
-          // every thread must be past its last read of the buffer being
-          // replaced, then the copy must be complete before anyone reads it
-          bufA ^= 1;
-          bufA_j = cur.j;
-          const TensorDesc *T = P.tensors + cur.j;
-          rowtabA = T->rowtab;
-          coltabA = T->coltab;
-          tc::bar_sync(bar_id, 128);
-          const uint4 *src =
-              reinterpret_cast<const uint4 *>(reinterpret_cast<const PrepImage *>(P.prep) + cur.j);
-          uint4 *dst = reinterpret_cast<uint4 *>(&S.img[wg][bufA]);
-          for (int i = row; i < (int)(sizeof(PrepImage) / 16); i += 128) dst[i] = __ldg(src + i);
-          tc::fence_proxy_async_smem();
-          tc::bar_sync(bar_id, 128);
-        }
-        const uint4 *rt = reinterpret_cast<const uint4 *>(rowtabA + cur.a * kRowTab);
-        const uint4 *ct = reinterpret_cast<const uint4 *>(coltabA + cur.b * kRowTab);
-        rt0 = __ldg(rt); rth = __ldg(rt + 2); rtl = __ldg(rt + 3);
-        ct0 = __ldg(ct); cth = __ldg(ct + 2); ctl = __ldg(ct + 3);
-      }
-      // ---- stage B (tile k-1): layer-1 epilogue -> A2 --------------------
-      if (hasBC) {
-        tc::mbar_wait(&S.acc1_full[wg], par);
-        tc::fence_after_sync();
-        const float sdown = S.img[wg][prev.buf].s2_down;
-#pragma unroll
-        for (int half = 0; half < 2; half++) {
-          uint32_t lo[16], hi[16];
-          tc::tmem_ld16(cbase + kACC1 + 16 * half, lo);        // x_hi*W_hi + x_lo*W_hi
-          tc::tmem_ld16(cbase + kACC1 + 32 + 16 * half, hi);   // x_hi*W_lo
-          tc::tmem_ld_wait();
-          uint32_t ah[8], al[8];
-#pragma unroll
-          for (int q = 0; q < 8; q++) {
-            float2 h = fadd2(make_float2(__uint_as_float(lo[2 * q]), __uint_as_float(lo[2 * q + 1])),
-                             make_float2(__uint_as_float(hi[2 * q]), __uint_as_float(hi[2 * q + 1])));
-            if (sdown != 1.0f) {
-              h.x *= sdown;
-              h.y *= sdown;
-            }
-            relu_split_f16(h.x, h.y, ah[q], al[q]);
-          }
-          tc::tmem_st8(cbase + kA2 + 8 * half, ah);
-          tc::tmem_st8(cbase + kA2 + 16 + 8 * half, al);
-        }
-        tc::tmem_st_wait();
-        tc::fence_before_sync();
-        if (row == 0) S.a2_buf[wg] = (uint32_t)prev.buf;
-        mbar_arrive(&S.a2_ready[wg]);
-      }
-      // ---- stage A (tile k): features -> A1, advanced state --------------
-      if (hasA) {
-        const PrepImage &im = S.img[wg][bufA];
-        FastIn x;
-        x.w = cur.w;
-        advance(cur.g, cur.s, adv, P.beta, x);
-        // the accumulators do not depend on the MLP: store them right away
-        if (cur.valid && !adv) *cur.sp = make_float4(x.m1, x.m2, x.m3, x.v);
-        const float rc[3] = {__uint_as_float(rt0.x), __uint_as_float(rt0.y), __uint_as_float(rt0.z)};
-        const float cc[3] = {__uint_as_float(ct0.x), __uint_as_float(ct0.y), __uint_as_float(ct0.z)};
-        const float sq[3] = {im.sqmr[0], im.sqmr[1], im.sqmr[2]};
-        float f[16];
-        fast_features(x, rc, cc, sq, f);
-        // normalize (features.py:349-354) so every operand fits fp16
-#pragma unroll
-        for (int q = 0; q < 16; q++) f[q] *= im.escale[q];
-        uint32_t a[16];
-        // slice s: [hi pairs of features 8s..8s+7 | lo pairs]
-#pragma unroll
-        for (int s = 0; s < 2; s++)
-#pragma unroll
-          for (int q = 0; q < 4; q++)
-            tc::split_pair_f16(f[8 * s + 2 * q], f[8 * s + 2 * q + 1], a[8 * s + q], a[8 * s + 4 + q]);
-        tc::tmem_st16(cbase + kA1, a);
-        uint32_t xh = 0, xl = 0;
-        if (KIND == LOPT_VELO_MLP) tc::split_pair_f16(clip01(x.g) * im.escale[16], 0.0f, xh, xl);
-        uint32_t b[16];
-        b[0] = rth.x; b[1] = rth.y; b[2] = rth.z; b[3] = cth.x;          // r5 r6 r7 rr5 rr6 rr7 c5 c6
-        b[4] = rtl.x; b[5] = rtl.y; b[6] = rtl.z; b[7] = ctl.x;
-        b[8] = cth.y; b[9] = cth.z;                                      // c7 rc5 rc6 rc7
-        b[10] = (xh & 0xFFFFu) | 0x3C000000u;                            // clip_hi, fp16 1 (bias)
-        b[11] = 0u;
-        b[12] = ctl.y; b[13] = ctl.z; b[14] = xl & 0xFFFFu; b[15] = 0u;
-        tc::tmem_st16(cbase + kA1 + 16, b);
-        tc::tmem_st_wait();
-        tc::fence_before_sync();
-        if (row == 0) S.a1_buf[wg] = (uint32_t)bufA;
-        mbar_arrive(&S.a1_ready[wg]);
-      }
-      // ---- stage C (tile k-1): layer-2 epilogue, layer 3, update ---------
-      if (hasBC) {
-        tc::mbar_wait(&S.acc2_full[wg], par);
-        tc::fence_after_sync();
-        if (prev.j != red.j) {
-          red.flush(P);
-          red.j = prev.j;
-          red.maxabs = 0.0f;
-          red.bad = 0;
-        }
-        const PrepImage &im = S.img[wg][prev.buf];
-        const float sup = im.s2_up;
-        float2 d2 = make_float2(im.b3[0], 0.0f), m2 = make_float2(im.b3[1], 0.0f);
-        const float4 *w30 = reinterpret_cast<const float4 *>(im.w3[0]);
-        const float4 *w31 = reinterpret_cast<const float4 *>(im.w3[1]);
-        const float4 *bb2 = reinterpret_cast<const float4 *>(im.b2f);
-#pragma unroll
-        for (int half = 0; half < 2; half++) {
-          uint32_t h2[16];
-          tc::tmem_ld16(cbase + kACC2 + 16 * half, h2);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const float4 wa = w30[4 * half + q], wb = w31[4 * half + q], bq = bb2[4 * half + q];
-            const float2 h01 = make_float2(fmaxf(fmaf(__uint_as_float(h2[4 * q]), sup, bq.x), 0.0f),
-                                           fmaxf(fmaf(__uint_as_float(h2[4 * q + 1]), sup, bq.y), 0.0f));
-            const float2 h23 = make_float2(fmaxf(fmaf(__uint_as_float(h2[4 * q + 2]), sup, bq.z), 0.0f),
-                                           fmaxf(fmaf(__uint_as_float(h2[4 * q + 3]), sup, bq.w), 0.0f));
-            d2 = ffma2(h01, make_float2(wa.x, wa.y), d2);
-            d2 = ffma2(h23, make_float2(wa.z, wa.w), d2);
-            m2 = ffma2(h01, make_float2(wb.x, wb.y), m2);
-            m2 = ffma2(h23, make_float2(wb.z, wb.w), m2);
-          }
-        }
-        const float dir = d2.x + d2.y, mag = m2.x + m2.y;
-        // engine.py:537-539, exp on the SFU (fp32 tolerance path)
-        const float ex = exp2f(mag * alpha_log2e);
-        const float du = ds * ((dir * ex) * beta_out);
-        float out = prev.w + du;
-        if (prev.valid) {
-          red.maxabs = fmaxf(red.maxabs, fabsf(du));
-          red.bad |= !isfinite(out);
-          if (apply_decay) out *= decay;   // optim.py:100-101
-          *prev.theta = out;
-        }
-      }
-      // ---- shift the pipeline ---------------------------------------------
-      if (hasA) {
-        prev.buf = bufA;
-        prev.j = cur.j;
-        prev.valid = cur.valid;
-        prev.w = cur.w;
-        prev.theta = cur.tp;
-        cur = nxt;
-      }
-    }
-    red.flush(P);
+  const uint32_t lane_addr = (uint32_t)((warp & 3) * 32) << 16;
+  if (warp >= kWarpC && warp < kWarpC + 4) {
+    // the constant slice that selects the layer-2 bias: fp16 {1, 1, 0, ...}
+    const uint32_t one[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    tc::tmem_st8(tbase + lane_addr + kOneCol, one);
+    tc::tmem_st_wait();
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == kIssueWarp0) tc::tmem_dealloc(tbase, kTmemCols);
+  tc::fence_after_sync();
+  const bool aborted = *P.abort_flag != 0;
+  const int32_t tb = (int32_t)(P.n_tiles * blockIdx.x / gridDim.x);
+  const int32_t te = (int32_t)(P.n_tiles * (blockIdx.x + 1) / gridDim.x);
+  const int32_t nt = aborted ? 0 : te - tb;
+
+  if (warp >= kWarpProducer && warp < kWarpProducer + kRoleWGs) {
+    // -------------------------------------------------------------- producers
+    // Producer p stages the tiles of parity p; both walk every tile so they
+    // agree on the tensor sequence (image buffer k % kImgs for the k-th
+    // tensor of this CTA's range).  The producer whose tile opens a tensor
+    // loads its operand image once the C warps are done with the buffer.
+    const int p = warp - kWarpProducer;
+    if (tc::elect_one() && nt > 0) {
+      Producer pr;
+      pr.seek(P, tb);
+      int k = -1, img = 0, cur_j = -1;
+      uint32_t par_bits = 0;
+      int32_t first0 = 0, first1 = 0, first2 = 0, first3 = 0;   // first tile of the tensor in buffer b
+      Cursor<kRing> rc;
+      for (int32_t i = 0; i < nt; i++) {
+        if (pr.j != cur_j) {
+          cur_j = pr.j;
+          k++;
+          img = k & (kImgs - 1);
+          const int32_t pf = img == 0 ? first0 : img == 1 ? first1 : img == 2 ? first2 : first3;
+          const int nb = (k + 1) & (kImgs - 1);   // buffer of tensor k - 3
+          const int32_t nf = nb == 0 ? first0 : nb == 1 ? first1 : nb == 2 ? first2 : first3;
+          if (img == 0) first0 = i; else if (img == 1) first1 = i; else if (img == 2) first2 = i; else first3 = i;
+          if (k >= kImgs) par_bits ^= 1u << img;
+          if ((i & 1) == p) {
+            if (k >= kImgs) {
+              // tensor k - kImgs used tiles [pf, nf - 1]: every C warp must be
+              // past the last tile of its parity in that range
+              const int32_t last = nf - 1;
+              for (int w = 0; w < kRoleWGs; w++) {
+                const int32_t need = ((last & 1) == w) ? last : last - 1;
+                if (need < pf) continue;
+                for (int q = 0; q < 4; q++) {
+                  int32_t d;
+                  while (true) {
+                    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];\n"
+                                 : "=r"(d)
+                                 : "r"(tc::smem_u32(&S.c_done[w][q]))
+                                 : "memory");
+                    if (d >= need) break;
+                    __nanosleep(32);
+                  }
+                }
+              }
+            }
+            mbar_arrive_tx(&S.img_full[img], (uint32_t)sizeof(PrepImage));
+            bulk_g2s(&S.img[img], reinterpret_cast<const PrepImage *>(P.prep) + pr.j,
+                     (uint32_t)sizeof(PrepImage), &S.img_full[img]);
+          }
+        }
+        if ((i & 1) == p) {
+          if (rc.wrapped) WAIT(&S.data_free[rc.i], rc.phase ^ 1u, 1);
+          trace(P, i, 0);
+          pr.stage(S.stage[rc.i], &S.full[rc.i], img, (int)((par_bits >> img) & 1u), P.dbg);
+        }
+        pr.advance(P);
+        rc.next();
+      }
+    }
+    __syncwarp();
+  } else if (warp == kWarpMma1 || warp == kWarpMma2) {
+    // --------------------------------------------------------------- MMA warps
+    const bool l1 = warp == kWarpMma1;
+    const uint32_t one = tbase + kOneCol;
+    Cursor<kRing> rc;
+    Cursor<kSlots> sc;
+    for (int32_t i = 0; i < nt; i++) {
+      WAIT(l1 ? &S.op_ready[sc.i] : &S.h_ready[sc.i], sc.phase, 4);
+      tc::fence_after_sync();
+      trace(P, i, l1 ? 3 : 5);
+      const PrepImage &im = S.img[S.stage[rc.i].meta.img];
+      const uint32_t op = tbase + 64 * sc.i, acc = op + 32;
+      if (tc::elect_one()) {
+        if (P.dbg & 1) tc::mma_commit(l1 ? &S.acc1_full[sc.i] : &S.acc2_full[sc.i]);
+        else if (l1) issue_layer1(im, op, acc, &S.acc1_full[sc.i]);
+        else issue_layer2(im, op, acc, one, &S.acc2_full[sc.i]);
+      }
+      __syncwarp();
+      rc.next();
+      sc.next();
+    }
+  } else if (warp < kWarpB) {
+    // ------------------------------------------ WG_A: features -> E/B operands
+    const int r0 = (warp - kWarpA) >> 2;
+    const bool adv = P.state_advanced != 0;
+    const float *beta = P.beta;
+    int32_t col_j = -1, col_b0 = -1;   // rowblock: cached column entry of this lane
+    Entry ce;
+    Stride<kRing> rc(r0);
+    Stride<kSlots> sc(r0);
+    for (int32_t i = r0; i < nt; i += kRoleWGs) {
+      WAIT(&S.full[rc.i], rc.phase, 5);
+      if (warp == 0) trace(P, i, 1);
+      const Stage &st = S.stage[rc.i];
+      const TileMeta &mt = st.meta;
+      const int32_t flags = mt.flags;
+      const bool valid = row >= mt.v0 && row < mt.v1;
+      WAIT(&S.img_full[mt.img], (uint32_t)mt.img_par, 9);
+      const PrepImage &im = S.img[mt.img];
+      float4 *sp = mt.state + row;
+      float w, g;
+      float4 sq4;
+      if (!(flags & kFlagSlow)) {
+        w = st.th[row];
+        g = st.gr[row];
+        sq4 = st.st[row];
+      } else {
+        w = valid ? mt.theta[row] : 0.0f;
+        g = valid ? mt.grad[row] : 0.0f;
+        sq4 = valid ? *sp : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      Entry re;
+      if (flags & kFlagRowblock) {
+        const uint4 v = st.rowent[0], hh = st.rowent[2], ll = st.rowent[3];
+        re.x[0] = __uint_as_float(v.x); re.x[1] = __uint_as_float(v.y); re.x[2] = __uint_as_float(v.z);
+        re.hi[0] = hh.x; re.hi[1] = hh.y; re.hi[2] = hh.z;
+        re.lo[0] = ll.x; re.lo[1] = ll.y; re.lo[2] = ll.z;
+        if (mt.j != col_j || mt.b0 != col_b0) {
+          col_j = mt.j;
+          col_b0 = mt.b0;
+          load_entry(mt.coltab, mt.b0 + row, ce);
+        }
+      } else {
+        const int32_t ec = mt.e0 + (valid ? row : (mt.v1 > mt.v0 ? mt.v0 : 0));
+        const int32_t la = (int32_t)((uint32_t)ec / (uint32_t)mt.n);
+        load_entry(mt.rowtab, la, re);
+        load_entry(mt.coltab, ec - la * mt.n, ce);
+        col_j = -1;
+      }
+      FastIn x;
+      x.w = w;
+      advance(g, sq4, adv, beta, x);
+      // the accumulators do not depend on the MLP: store them right away
+      if (valid && !adv) *sp = make_float4(x.m1, x.m2, x.m3, x.v);
+      const float sq[3] = {im.sqmr[0], im.sqmr[1], im.sqmr[2]};
+      float f[16];
+      fast_features(x, re.x, ce.x, sq, f);
+      // normalize (features.py:349-354) so every operand fits fp16
+      const float4 *es = reinterpret_cast<const float4 *>(im.escale);
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const float4 e4 = es[q];
+        const float2 p0 = fmul2(make_float2(f[4 * q], f[4 * q + 1]), make_float2(e4.x, e4.y));
+        const float2 p1 = fmul2(make_float2(f[4 * q + 2], f[4 * q + 3]), make_float2(e4.z, e4.w));
+        f[4 * q] = p0.x; f[4 * q + 1] = p0.y; f[4 * q + 2] = p1.x; f[4 * q + 3] = p1.y;
+      }
+      uint32_t ev[16];   // E_hi(8) E_lo(8)
+#pragma unroll
+      for (int q = 0; q < 8; q++) split2(f[2 * q], f[2 * q + 1], ev[q], ev[8 + q]);
+      uint32_t xh = 0, xl = 0;
+      if (KIND == LOPT_VELO_MLP) split2(clip01(x.g) * im.escale[16], 0.0f, xh, xl);
+      uint32_t bv[16];   // B_hi(8) B_lo(8)
+      bv[0] = re.hi[0]; bv[1] = re.hi[1]; bv[2] = re.hi[2];
+      bv[3] = ce.hi[0]; bv[4] = ce.hi[1]; bv[5] = ce.hi[2];
+      bv[6] = (xh & 0xFFFFu) | 0x3C000000u;   // clip_hi, fp16 1 (bias)
+      bv[7] = 0u;
+      bv[8] = re.lo[0]; bv[9] = re.lo[1]; bv[10] = re.lo[2];
+      bv[11] = ce.lo[0]; bv[12] = ce.lo[1]; bv[13] = ce.lo[2];
+      bv[14] = xl & 0xFFFFu;
+      bv[15] = 0u;
+      // TMEM slot is free once C has read the tile kSlots before
+      if (sc.wrapped) WAIT(&S.slot_free[sc.i], sc.phase ^ 1u, 6);
+      tc::fence_after_sync();
+      const uint32_t ta = tbase + lane_addr + 64 * sc.i;
+      if (!(P.dbg & 2)) {
+        tc::tmem_st16(ta, ev);
+        tc::tmem_st16(ta + 16, bv);
+      }
+      tc::tmem_st_wait();
+      tc::fence_before_sync();
+      if (warp == 0) trace(P, i, 2);
+      warp_arrive(&S.op_ready[sc.i]);
+      rc.next();
+      sc.next();
+    }
+  } else if (warp < kWarpC) {
+    // ------------------------------------------- WG_B: layer-1 epilogue -> H
+    const int r0 = (warp - kWarpB) >> 2;
+    Stride<kRing> rc(r0);
+    Stride<kSlots> sc(r0);
+    for (int32_t i = r0; i < nt; i += kRoleWGs) {
+      WAIT(&S.full[rc.i], rc.phase, 5);
+      const int img = S.stage[rc.i].meta.img;
+      WAIT(&S.acc1_full[sc.i], sc.phase, 7);
+      tc::fence_after_sync();
+      // the image is read only after acc1_full: A waited for its load before
+      // the MMAs of this tile were issued
+      const float sdown = S.img[img].s2_down;
+      if (warp == kWarpB) trace(P, i, 4);
+      const uint32_t ta = tbase + lane_addr + 64 * sc.i;
+#pragma unroll
+      for (int half = 0; half < 2; half++) {
+        uint32_t h[16];
+        if (P.dbg & 2) {
+#pragma unroll
+          for (int q = 0; q < 16; q++) h[q] = __float_as_uint((float)(q + i));
+        } else {
+          tc::tmem_ld16(ta + 32 + 16 * half, h);
+          tc::tmem_ld_wait();
+        }
+        if (sdown != 1.0f) {
+#pragma unroll
+          for (int q = 0; q < 16; q++) h[q] = __float_as_uint(__uint_as_float(h[q]) * sdown);
+        }
+        uint32_t hi[8], lo[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          relu_split2(__uint_as_float(h[2 * q]), __uint_as_float(h[2 * q + 1]), hi[q], lo[q]);
+        if (!(P.dbg & 2)) {
+          tc::tmem_st8(ta + 8 * half, hi);
+          tc::tmem_st8(ta + 16 + 8 * half, lo);
+        }
+      }
+      tc::tmem_st_wait();
+      tc::fence_before_sync();
+      warp_arrive(&S.h_ready[sc.i]);
+      rc.next();
+      sc.next();
+    }
+  } else if (warp < kWarpProducer) {
+    // ------------------------- WG_C: layer-2 epilogue, layer 3, update, store
+    const int r0 = (warp - kWarpC) >> 2;
+    const float alpha_log2e = P.alpha * 1.4426950408889634f;
+    const float dsb = P.step->ds * P.beta_out;
+    const float decay = P.step->apply_decay != 0 ? P.step->decay : 1.0f;
+    int red_j = -1;
+    float red_max = 0.0f, red_out = 0.0f;   // max |delta|, NaN-propagating max |theta'|
+    Stride<kRing> rc(r0);
+    Stride<kSlots> sc(r0);
+    for (int32_t i = r0; i < nt; i += kRoleWGs) {
+      WAIT(&S.full[rc.i], rc.phase, 5);
+      const Stage &st = S.stage[rc.i];
+      const TileMeta &mt = st.meta;
+      const int j = mt.j;
+      if (j != red_j) {
+        if (red_j >= 0) {
+          if (red_max > 0.0f)
+            atomicMax(reinterpret_cast<unsigned int *>(&P.maxabs[red_j]), __float_as_uint(red_max));
+          if (!(red_out <= 3.402823466e38f)) atomicOr(&P.status[red_j], LOPT_STATUS_NONFINITE_PARAM);
+        }
+        red_j = j;
+        red_max = 0.0f;
+        red_out = 0.0f;
+      }
+      const bool valid = row >= mt.v0 && row < mt.v1;
+      float *tp = mt.theta + row;
+      const float w = (mt.flags & kFlagSlow) ? (valid ? *tp : 0.0f) : st.th[row];
+      const PrepImage &ip = S.img[mt.img];
+      WAIT(&S.acc2_full[sc.i], sc.phase, 8);
+      tc::fence_after_sync();
+      if (warp == kWarpC) trace(P, i, 6);
+      uint32_t h2[32];
+      if (P.dbg & 2) {
+#pragma unroll
+        for (int q = 0; q < 32; q++) h2[q] = __float_as_uint(w * (float)q);
+      } else {
+        tc::tmem_ld32(tbase + lane_addr + 64 * sc.i + 32, h2);
+      }
+      tc::tmem_ld_wait();
+      tc::fence_before_sync();
+      warp_arrive(&S.slot_free[sc.i]);
+      // layer 3 in f32: four independent FFMA2 chains
+      float2 d0 = make_float2(ip.b3[0], 0.0f), d1 = make_float2(0.0f, 0.0f);
+      float2 m0 = make_float2(ip.b3[1], 0.0f), m1 = make_float2(0.0f, 0.0f);
+      const float4 *w3 = reinterpret_cast<const float4 *>(ip.w3i);
+#pragma unroll
+      for (int q = 0; q < 16; q += 2) {
+        const float4 wa = w3[q], wb = w3[q + 1];
+        const float2 ha = make_float2(fmaxf(__uint_as_float(h2[2 * q]), 0.0f),
+                                      fmaxf(__uint_as_float(h2[2 * q + 1]), 0.0f));
+        const float2 hb = make_float2(fmaxf(__uint_as_float(h2[2 * q + 2]), 0.0f),
+                                      fmaxf(__uint_as_float(h2[2 * q + 3]), 0.0f));
+        d0 = ffma2(ha, make_float2(wa.x, wa.y), d0);
+        m0 = ffma2(ha, make_float2(wa.z, wa.w), m0);
+        d1 = ffma2(hb, make_float2(wb.x, wb.y), d1);
+        m1 = ffma2(hb, make_float2(wb.z, wb.w), m1);
+      }
+      // the data slot (theta, meta) and the image are no longer needed
+      warp_arrive(&S.data_free[rc.i]);
+      if ((threadIdx.x & 31) == 0)
+        asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&S.c_done[r0][warp & 3])),
+                     "r"(i)
+                     : "memory");
+      const float dir = (d0.x + d0.y) + (d1.x + d1.y), mag = (m0.x + m0.y) + (m1.x + m1.y);
+      // engine.py:537-539, exp on the SFU (fp32 tolerance path)
+      const float du = dsb * (dir * ex2_ftz(mag * alpha_log2e));
+      const float out = (w + du) * decay;   // optim.py:100-101 (decay = 1 without weight decay)
+      if (valid) {
+        red_max = fmaxf(red_max, fabsf(du));
+        red_out = max_nan_abs(red_out, out);
+        *tp = out;
+      }
+      rc.next();
+      sc.next();
+    }
+    if (red_j >= 0) {
+      if (red_max > 0.0f)
+        atomicMax(reinterpret_cast<unsigned int *>(&P.maxabs[red_j]), __float_as_uint(red_max));
+      if (!(red_out <= 3.402823466e38f)) atomicOr(&P.status[red_j], LOPT_STATUS_NONFINITE_PARAM);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, kTmemCols);
 }
 
 static int g_num_sms = 0;
 
-void launch_tc_apply(const DevicePlan &P, cudaStream_t s) {
+void launch_tc_apply(const DevicePlan &P0, cudaStream_t s) {
+  DevicePlan P = P0;
+  if (const char *d = getenv("LOPT_APPLY_DEBUG")) P.dbg = atoi(d);   // timing experiments
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
-  // more than half of the SM's shared memory: one CTA per SM, which the
-  // 512-column TMEM allocation needs anyway
-  const size_t smem = std::max<size_t>(sizeof(ApplySmem) + 1024, 120 * 1024);
-  const int grid = (int)std::min<int64_t>(g_num_sms, (P.n_tiles + kWGs - 1) / kWGs);
+  // one CTA per SM (the 512-column TMEM allocation needs it anyway)
+  const size_t smem = sizeof(ApplySmem) + 1024;
+  const int grid = (int)std::min<int64_t>(g_num_sms, P.n_tiles);
   if (P.kind == LOPT_SMALL_FC_LOPT) {
     cudaFuncSetAttribute(apply_tc_kernel<LOPT_SMALL_FC_LOPT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -446,3 +764,10 @@ void launch_tc_apply(const DevicePlan &P, cudaStream_t s) {
 }
 
 }  // namespace lopt
+
+extern "C" int lopt_debug_apply_trace(long long *host, int32_t n) {
+  if (!host || n < 0 || n > lopt::kTraceTiles * 8) return LOPT_ERR_INVALID;
+  return cudaMemcpyFromSymbol(host, lopt::g_trace, sizeof(long long) * n) == cudaSuccess
+             ? LOPT_OK
+             : LOPT_ERR_CUDA;
+}

@@ -178,8 +178,18 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
     d.apply_item0 = (int32_t)p->aitems.size();
     d.tile0 = p->n_tiles;
     if (fast) {
-      // the persistent tensor-core kernel walks 128-element tiles implicitly
-      p->n_tiles += (t.hi - t.lo + apply_chunk - 1) / apply_chunk;
+      // the persistent tensor-core kernel walks 128-lane tiles implicitly
+      int64_t tiles = 0;
+      if (t.hi > t.lo && t.n % apply_chunk == 0) {
+        d.rowblock = 1;
+        d.a_lo = (int32_t)(t.lo / t.n);
+        d.m_rows = (int32_t)((t.hi - 1) / t.n - t.lo / t.n + 1);
+        tiles = (int64_t)d.m_rows * (t.n / apply_chunk);
+      } else {
+        tiles = (t.hi - t.lo + apply_chunk - 1) / apply_chunk;
+      }
+      d.tiles = (int32_t)tiles;
+      p->n_tiles += tiles;
     } else {
       for (int64_t e = t.lo; e < t.hi; e += apply_chunk)
         p->aitems.push_back(ChunkItem{j, 0, e, std::min<int64_t>(t.hi, e + apply_chunk)});

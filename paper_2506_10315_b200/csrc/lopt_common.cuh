@@ -44,8 +44,13 @@ struct TensorDesc {
   int32_t weight_slot;
   int32_t stat_item0, stat_items;   // phase-1 items of this tensor (contiguous)
   int32_t apply_item0, apply_items; // phase-2 items of this tensor (contiguous)
-  int32_t pad_;
-  int64_t tile0;          // fast path: first 128-element tile of this tensor
+  int32_t tiles;          // fast path: 128-lane tiles of this tensor
+  int64_t tile0;          // fast path: first tile of this tensor in the plan
+  // fast path tile shape: rowblock = 1 when n % 128 == 0; then tile q is row
+  // a_lo + q % m_rows, columns [128 * (q / m_rows), +128) (column-block major,
+  // so a run of tiles shares its column-table entries); otherwise tile q is
+  // the flat elements [lo + 128 q, +128)
+  int32_t rowblock, a_lo, m_rows, pad_;
 };
 
 // Phase-0 tile: rows [a0, a1) x columns [b0, b1) of one tensor.
@@ -102,6 +107,7 @@ struct DevicePlan {
   int64_t n_tiles;        // 128-element tiles over all tensors
   unsigned char *prep;    // per-tensor PrepImage (B operands, layer-3 weights)
   double *bcsum;          // [count x d_feat] closed-form sums of broadcast features
+  int32_t dbg, pad_dbg;   // timing experiments only (LOPT_APPLY_DEBUG), 0 in production
 };
 
 __host__ __device__ inline int weight_stride(int d, int h1, int h2) {

@@ -89,26 +89,27 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
     s2s[1] = ldexpf(1.0f, s2);
   }
   __syncthreads();
-  // layer 1, N-packed (see PrepImage): slice s holds eight features q[s][0..7]
-  for (int i = threadIdx.x; i < 4 * 32 * 8; i += blockDim.x) {
-    const int s = i >> 8, o = (i >> 3) & 31, q = i & 7;
+  // layer 1 (see PrepImage): slices 0/1 = W1_hi/W1_lo over the per-element
+  // features, slices 2/3 over the broadcast slice [12 row/col | clip | 1 | 0 0]
+  for (int i = threadIdx.x; i < 2 * 32 * 16; i += blockDim.x) {
+    const int s = i >> 9, o = (i >> 4) & 31, q = i & 15;
     float v = 0.0f;
-    if (s < 2) {
-      v = w1[o * D + elem_col(KIND, 8 * s + q)];
-    } else if (s == 2) {
-      v = w1[o * D + bc_col(q)];                       // r5 r6 r7 rr5 rr6 rr7 c5 c6
-    } else {
-      if (q < 4) v = w1[o * D + bc_col(8 + q)];        // c7 rc5 rc6 rc7
-      else if (q == 4) v = (KIND == LOPT_VELO_MLP) ? w1[o * D + 28] : 0.0f;   // clip
-      else if (q == 5) v = bias1[o];                   // the constant-1 column
+    if (s == 0) {
+      v = w1[o * D + elem_col(KIND, q)];
+    } else if (q < 12) {
+      v = w1[o * D + bc_col(q)];
+    } else if (q == 12) {
+      v = (KIND == LOPT_VELO_MLP) ? w1[o * D + 28] : 0.0f;   // clip(g)
+    } else if (q == 13) {
+      v = bias1[o];                                          // the constant-1 column
     }
     uint16_t hi, lo;
     split1(v, hi, lo);
-    img->b1[s][bslot(o, q, 64)] = hi;            // x_hi * W_hi
-    img->b1[s][bslot(o, 8 + q, 64)] = hi;        // x_lo * W_hi
-    img->b1[s][bslot(32 + o, q, 64)] = lo;       // x_hi * W_lo
-    img->b1[s][bslot(32 + o, 8 + q, 64)] = 0;
+    img->b1[2 * s][bslot(o, q)] = hi;
+    img->b1[2 * s + 1][bslot(o, q)] = lo;
   }
+  // layer 2: W2 hi/lo by K halves, then the bias slice (k = 0: hi, k = 1: lo)
+  const float sd = s2s[0], su = s2s[1];
   for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
     const int o = i >> 5, k = i & 31;
     uint16_t hi, lo;
@@ -116,16 +117,25 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
     img->b2[k >> 4][bslot(o, k & 15)] = hi;
     img->b2[2 + (k >> 4)][bslot(o, k & 15)] = lo;
   }
-  if (threadIdx.x < 32) img->b2f[threadIdx.x] = b2[threadIdx.x];
-  if (threadIdx.x < 64) img->w3[threadIdx.x >> 5][threadIdx.x & 31] = w3[threadIdx.x];
+  for (int i = threadIdx.x; i < 32 * 16; i += blockDim.x) {
+    const int o = i >> 4, k = i & 15;
+    uint16_t hi, lo;
+    split1(b2[o] * sd, hi, lo);
+    img->b2[4][bslot(o, k)] = k == 0 ? hi : (k == 1 ? lo : (uint16_t)0);
+  }
+  if (threadIdx.x < 64) {
+    const int o = threadIdx.x & 31, out = threadIdx.x >> 5;
+    img->w3i[o >> 1][2 * out + (o & 1)] = w3[out * 32 + o] * su;
+  }
   if (threadIdx.x < 2) img->b3[threadIdx.x] = b3[threadIdx.x];
   if (threadIdx.x < 3) img->sqmr[threadIdx.x] = sqrtf(P.tscal[j].mr[threadIdx.x]);
   if (threadIdx.x < 17)
     img->escale[threadIdx.x] = threadIdx.x < 16 ? scale[elem_col(KIND, threadIdx.x)]
                                                 : (KIND == LOPT_VELO_MLP ? scale[28] : 0.0f);
+  if (threadIdx.x >= 17 && threadIdx.x < 20) img->escale[threadIdx.x] = 0.0f;
   if (threadIdx.x == 0) {
-    img->s2_down = s2s[0];
-    img->s2_up = s2s[1];
+    img->s2_down = sd;
+    img->pad[0] = img->pad[1] = 0.0f;
   }
   // broadcast operands: rows r5 r6 r7 rr5 rr6 rr7, columns c5 c6 c7 rc5 rc6 rc7
   const float rs[6] = {scale[4], scale[5], scale[6], scale[14], scale[15], scale[16]};

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(128) umma_selftest_kernel(int a_in_tmem, int f
 // (M=128, N=32, K=16, f16, A in TMEM): `batch` MMAs per commit, `rounds`
 // commit->wait round trips, cycles reported per round in out[0].
 __global__ void __launch_bounds__(128) umma_probe_kernel(int batch, int rounds, int N, int a_smem,
-                                                         int issuers, long long *out) {
+                                                         int issuers, int rotate, int warp_wide, long long *out) {
   __shared__ __align__(1024) uint16_t Bs[256 * 16];
   __shared__ __align__(1024) uint16_t As[128 * 16];
   __shared__ __align__(8) uint64_t mbar;
@@ -104,17 +104,49 @@ __global__ void __launch_bounds__(128) umma_probe_kernel(int batch, int rounds, 
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t base = tbase;
+  if (warp_wide) {
+    // `issuers` converged warps, each issuing through elect.sync into its own
+    // accumulator columns, descriptors hoisted out of the loop
+    if (warp < issuers) {
+      const uint32_t idesc = tc::idesc_f16_f32(128, N);
+      const uint64_t bdesc = tc::smem_desc_kmajor(tc::smem_u32(Bs), N * 16, 128);
+      const uint64_t adesc = tc::smem_desc_kmajor(tc::smem_u32(As), 2048, 128);
+      const uint32_t d = base + 64 * warp;
+      long long t0 = clock64();
+      for (int r = 0; r < rounds; r++) {
+        if (tc::elect_one()) {
+          for (int b = 0; b < batch; b++) {
+            if (a_smem) tc::mma_ss(d, adesc, bdesc, idesc, b > 0);
+            else tc::mma_ts(d, base + 256, bdesc, idesc, b > 0);
+          }
+          tc::mma_commit(&mbars[warp]);
+        }
+        __syncwarp();
+        tc::mbar_wait(&mbars[warp], r & 1);
+      }
+      long long t1 = clock64();
+      if ((t & 31) == 0) out[warp] = (t1 - t0) / rounds;
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(base, 512);
+    return;
+  }
   if (issuers > 1) {
     // `issuers` warps, lane 0 of each issuing its own MMA stream into its
     // own accumulator columns: does MMA throughput scale with issuers?
     if ((t & 31) == 0 && warp < issuers) {
-      const uint32_t idesc = tc::idesc_f16_f32(128, 64);
-      const uint64_t bdesc = tc::smem_desc_kmajor(tc::smem_u32(Bs), 64 * 16, 128);
+      const uint32_t idesc = tc::idesc_f16_f32(128, N);
+      const uint64_t bdesc = tc::smem_desc_kmajor(tc::smem_u32(Bs), N * 16, 128);
+      const uint64_t adesc = tc::smem_desc_kmajor(tc::smem_u32(As), 2048, 128);
       const uint32_t d = base + 64 * warp;
       long long t0 = clock64();
       for (int r = 0; r < rounds; r++) {
 #pragma unroll 1
-        for (int b = 0; b < batch; b++) tc::mma_ts(d, base + 256, bdesc, idesc, b > 0);
+        for (int b = 0; b < batch; b++) {
+          if (a_smem) tc::mma_ss(d, adesc, bdesc, idesc, b > 0);
+          else tc::mma_ts(d, base + 256, bdesc, idesc, b > 0);
+        }
         tc::mma_commit(&mbars[warp]);
         tc::mbar_wait(&mbars[warp], r & 1);
       }
@@ -134,6 +166,7 @@ __global__ void __launch_bounds__(128) umma_probe_kernel(int batch, int rounds, 
     for (int r = 0; r < rounds; r++) {
       for (int b = 0; b < batch; b++) {
         if (a_smem) tc::mma_ss(base, adesc, bdesc, idesc, b > 0);
+        else if (rotate) tc::mma_ts(base + (uint32_t)((b & 3) * 64), base + 256, bdesc, idesc, b > 3);
         else tc::mma_ts(base, base + 256, bdesc, idesc, b > 0);
       }
       tc::mma_commit(&mbar);
@@ -169,10 +202,10 @@ extern "C" int lopt_probe_umma(int32_t batch, int32_t rounds, long long *out, vo
   // bits 16..27 = N (default 32); bit 28 = A from shared memory
   const int b = batch & 0xFFF, N = (batch >> 16) & 0xFFF ? (batch >> 16) & 0xFFF : 32;
   const int issuers = (batch >> 12) & 7 ? (batch >> 12) & 7 : 1;
-  const int a_smem = (batch >> 28) & 1;
+  const int a_smem = (batch >> 28) & 1, rotate = (batch >> 29) & 1, warp_wide = (batch >> 30) & 1;
   if (N < 16 || N > 256 || N % 16 || issuers > 4) return LOPT_ERR_INVALID;
   lopt::umma_probe_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(b, rounds, N, a_smem, issuers,
-                                                               out);
+                                                               rotate, warp_wide, out);
   return cudaGetLastError() == cudaSuccess ? LOPT_OK : LOPT_ERR_CUDA;
 }
 

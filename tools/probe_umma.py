@@ -21,15 +21,35 @@ for a_smem in (0, 1):
             c = int(out[0].item())
             print(f"A={'smem' if a_smem else 'tmem'} N={N:3d} batch={batch:3d}: "
                   f"{c:6d} cycles/round {c / batch:7.1f} cycles/MMA")
-for issuers in (1, 2, 3, 4):
-    for batch in (8, 64):
-        out.zero_()
-        flags = batch | (issuers << 12) | (64 << 16)
-        if issuers == 1:
-            flags |= 0  # single-issuer path of the probe (N=64)
-        _lib.check(L.lopt_probe_umma(flags, 500, out.data_ptr(), s))
+for N in (32, 64, 128):
+    for batch in (16, 64):
+        flags = batch | (N << 16) | (1 << 29)
+        _lib.check(L.lopt_probe_umma(flags, 1000, out.data_ptr(), s))
         torch.cuda.synchronize()
-        c = [int(v) for v in out.tolist()[:issuers]]
-        mx = max(c)
-        print(f"issuers={issuers} N=64 batch={batch:3d}: max {mx} cycles/round per issuer, "
-              f"aggregate {mx / (batch * issuers):6.1f} cycles/MMA")
+        c = int(out[0].item())
+        print(f"A=tmem N={N:3d} batch={batch:3d} 4 independent accumulators: "
+              f"{c / batch:7.1f} cycles/MMA")
+for a_smem in (0, 1):
+    for N in (32, 64):
+        for issuers in (2, 3, 4):
+            for batch in (10, 64):
+                out.zero_()
+                flags = batch | (issuers << 12) | (N << 16) | (a_smem << 28)
+                _lib.check(L.lopt_probe_umma(flags, 500, out.data_ptr(), s))
+                torch.cuda.synchronize()
+                c = [int(v) for v in out.tolist()[:issuers]]
+                mx = max(c)
+                print(f"A={'smem' if a_smem else 'tmem'} issuers={issuers} N={N} batch={batch:3d}: "
+                      f"max {mx} cycles/round per issuer, aggregate {mx / (batch * issuers):6.1f} cycles/MMA")
+for a_smem in (0, 1):
+    for N in (32, 64, 128, 256):
+        for issuers in (1, 2, 4):
+            for batch in (10, 64):
+                out.zero_()
+                flags = batch | (issuers << 12) | (N << 16) | (a_smem << 28) | (1 << 30)
+                _lib.check(L.lopt_probe_umma(flags, 500, out.data_ptr(), s))
+                torch.cuda.synchronize()
+                c = [int(v) for v in out.tolist()[:issuers]]
+                mx = max(c)
+                print(f"WARP-WIDE A={'smem' if a_smem else 'tmem'} issuers={issuers} N={N} batch={batch:3d}: "
+                      f"max {mx} cycles/round, aggregate {mx / (batch * issuers):6.1f} cycles/MMA")

@@ -1,0 +1,41 @@
+"""Pipeline trace of the apply kernel (CTA 0, first 64 tiles): clock64 at
+producer stage (0), A data ready (1), A operands done (2), MMA1 go (3),
+B acc1 ready (4), MMA2 go (5), C acc2 ready (6).
+
+    LOPT_APPLY_DEBUG=32 python tools/trace_apply.py
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+os.environ.setdefault("LOPT_APPLY_DEBUG", "32")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2506_10315_b200 import LearnedOptimizer, _lib  # noqa: E402
+
+params, grads = bench.make_model("vit_b16", torch.device("cuda"))
+for p, g in zip(params, grads):
+    p.grad = g
+opt = LearnedOptimizer(params, feature_set="small_fc_lopt", mode="fast", check_errors=False)
+for _ in range(3):
+    opt.step()
+torch.cuda.synchronize()
+L = _lib.lib()
+buf = (ctypes.c_longlong * (64 * 8))()
+L.lopt_debug_apply_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+assert L.lopt_debug_apply_trace(ctypes.addressof(buf), 64 * 8) == 0
+t = np.array(buf[:], dtype=np.int64).reshape(64, 8)[:, :7]
+t = t - t[0, 0]
+names = ["prod", "A_in", "A_out", "mma1", "B_in", "mma2", "C_in"]
+print("tile " + " ".join(f"{n:>8s}" for n in names))
+for i in range(64):
+    print(f"{i:4d} " + " ".join(f"{v:8d}" for v in t[i]))
+d = np.diff(t[8:, :], axis=0).mean(axis=0)
+print("mean per-tile spacing (tiles 8..63):", " ".join(f"{n}={v:.0f}" for n, v in zip(names, d)))
+lat = (t[8:, 1:] - t[8:, :-1]).mean(axis=0)
+print("mean stage latency:", " ".join(f"{names[k]}->{names[k+1]}={v:.0f}" for k, v in enumerate(lat)))
