@@ -36,7 +36,8 @@ def flags():
         "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
         "-Xcompiler", "-fPIC", "-Xptxas", "-v" if os.environ.get("LOPT_PTXAS_VERBOSE") else "-O3",
         "-I", os.path.join(ROOT, "include"),
-    ] + (["-DLOPT_WATCHDOG"] if os.environ.get("LOPT_WATCHDOG") else [])
+    ] + (["-DLOPT_WATCHDOG"] if os.environ.get("LOPT_WATCHDOG") else []) + (
+        ["-DLOPT_TRACE"] if os.environ.get("LOPT_TRACE") else [])
 
 
 def _stale() -> bool:

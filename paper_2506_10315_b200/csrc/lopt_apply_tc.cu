@@ -31,6 +31,7 @@
 // Tiles of tensors with n % 128 == 0 are (row, 128-column block) pairs in
 // column-block-major order, so consecutive tiles share their column-table
 // entries (kept in WG_A's registers); other tensors use flat 128-element tiles.
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 
@@ -41,11 +42,14 @@ namespace lopt {
 constexpr int kRing = 16;      // smem tile slots (prefetch + in flight)
 constexpr int kSlots = 7;      // TMEM tile slots
 constexpr int kImgs = 4;       // smem operand images (tensor switches in flight)
-constexpr int kRoleWGs = 2;    // warpgroups per role (even / odd tiles)
-constexpr int kApplyThreads = 3 * kRoleWGs * 128 + (kRoleWGs + 2) * 32;
-constexpr int kWarpA = 0, kWarpB = 4 * kRoleWGs, kWarpC = 8 * kRoleWGs;
-constexpr int kWarpProducer = 12 * kRoleWGs;   // kRoleWGs producer warps (even / odd tiles)
-constexpr int kWarpMma1 = kWarpProducer + kRoleWGs, kWarpMma2 = kWarpMma1 + 1;
+// warpgroups per role (tile i goes to warpgroup i % kWGs of the role) and
+// producer warps (tile i staged by producer i % kProducers)
+constexpr int kWGsA = 2, kWGsB = 2, kWGsC = 2, kProducers = 2;
+constexpr int kApplyThreads = (kWGsA + kWGsB + kWGsC) * 128 + (kProducers + 2) * 32;
+constexpr int kWarpA = 0, kWarpB = 4 * kWGsA, kWarpC = kWarpB + 4 * kWGsB;
+constexpr int kWarpProducer = kWarpC + 4 * kWGsC;
+constexpr int kWarpMma1 = kWarpProducer + kProducers, kWarpMma2 = kWarpMma1 + 1;
+static_assert(kRing % kProducers == 0 && kRing % kWGsA == 0 && kRing % kWGsC == 0, "ring ownership");
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kOneCol = 64 * kSlots;   // shared constant slice
 static_assert(kOneCol + 8 <= kTmemCols, "TMEM budget");
@@ -89,7 +93,7 @@ struct __align__(1024) ApplySmem {
   uint64_t acc2_full[kSlots];  // MMA2 -> C (commit)
   uint64_t slot_free[kSlots];  // C -> A (one arrival per warp)
   uint64_t img_full[kImgs];    // producer -> A: operand image loaded (TMA complete_tx)
-  int32_t c_done[kRoleWGs][4]; // C warps: last tile finished (image-buffer reuse)
+  int32_t c_done[kWGsC][4];    // C warps: last tile finished (image-buffer reuse)
   uint32_t tmem_base;
 };
 
@@ -281,38 +285,40 @@ __device__ __forceinline__ void load_entry(const float *tab, int32_t i, Entry &E
   E.lo[0] = l.x; E.lo[1] = l.y; E.lo[2] = l.z;
 }
 
-__device__ __forceinline__ void issue_layer1(const PrepImage &im, uint32_t op, uint32_t acc, uint64_t *bar) {
-  const uint32_t idesc = tc::idesc_f16_f32(128, 32);
-  const uint64_t w_eh = tc::smem_desc_kmajor(tc::smem_u32(im.b1[0]), 512, 128);
-  const uint64_t w_el = tc::smem_desc_kmajor(tc::smem_u32(im.b1[1]), 512, 128);
-  const uint64_t w_bh = tc::smem_desc_kmajor(tc::smem_u32(im.b1[2]), 512, 128);
-  const uint64_t w_bl = tc::smem_desc_kmajor(tc::smem_u32(im.b1[3]), 512, 128);
-  const uint32_t d = acc;
-  tc::mma_ts(d, op + 0, w_eh, idesc, 0);
-  tc::mma_ts(d, op + 8, w_eh, idesc, 1);
-  tc::mma_ts(d, op + 0, w_el, idesc, 1);
-  tc::mma_ts(d, op + 16, w_bh, idesc, 1);
-  tc::mma_ts(d, op + 24, w_bh, idesc, 1);
-  tc::mma_ts(d, op + 16, w_bl, idesc, 1);
+// MMA issue.  `dimg` is the UMMA descriptor of the tile's operand image (its
+// first byte); every B slice is a constant 16-byte offset from it, so a tile
+// costs one uniform add per MMA instead of rebuilding descriptors.
+constexpr uint64_t slice_off(size_t bytes) { return (uint64_t)(bytes >> 4); }
+__device__ __forceinline__ void issue_layer1(uint64_t dimg, uint32_t op, uint32_t acc, uint64_t *bar) {
+  constexpr uint32_t idesc = tc::idesc_f16_f32(128, 32);
+  const uint64_t w_eh = dimg + slice_off(offsetof(PrepImage, b1[0]));
+  const uint64_t w_el = dimg + slice_off(offsetof(PrepImage, b1[1]));
+  const uint64_t w_bh = dimg + slice_off(offsetof(PrepImage, b1[2]));
+  const uint64_t w_bl = dimg + slice_off(offsetof(PrepImage, b1[3]));
+  tc::mma_ts(acc, op + 0, w_eh, idesc, 0);
+  tc::mma_ts(acc, op + 8, w_eh, idesc, 1);
+  tc::mma_ts(acc, op + 0, w_el, idesc, 1);
+  tc::mma_ts(acc, op + 16, w_bh, idesc, 1);
+  tc::mma_ts(acc, op + 24, w_bh, idesc, 1);
+  tc::mma_ts(acc, op + 16, w_bl, idesc, 1);
   tc::mma_commit(bar);
 }
 
-__device__ __forceinline__ void issue_layer2(const PrepImage &im, uint32_t op, uint32_t acc,
+__device__ __forceinline__ void issue_layer2(uint64_t dimg, uint32_t op, uint32_t acc,
                                              uint32_t one, uint64_t *bar) {
-  const uint32_t idesc = tc::idesc_f16_f32(128, 32);
-  const uint64_t h0 = tc::smem_desc_kmajor(tc::smem_u32(im.b2[0]), 512, 128);
-  const uint64_t h1 = tc::smem_desc_kmajor(tc::smem_u32(im.b2[1]), 512, 128);
-  const uint64_t l0 = tc::smem_desc_kmajor(tc::smem_u32(im.b2[2]), 512, 128);
-  const uint64_t l1 = tc::smem_desc_kmajor(tc::smem_u32(im.b2[3]), 512, 128);
-  const uint64_t bb = tc::smem_desc_kmajor(tc::smem_u32(im.b2[4]), 512, 128);
-  const uint32_t d = acc;
-  tc::mma_ts(d, op + 0, h0, idesc, 0);
-  tc::mma_ts(d, op + 8, h1, idesc, 1);
-  tc::mma_ts(d, op + 16, h0, idesc, 1);
-  tc::mma_ts(d, op + 24, h1, idesc, 1);
-  tc::mma_ts(d, op + 0, l0, idesc, 1);
-  tc::mma_ts(d, op + 8, l1, idesc, 1);
-  tc::mma_ts(d, one, bb, idesc, 1);
+  constexpr uint32_t idesc = tc::idesc_f16_f32(128, 32);
+  const uint64_t h0 = dimg + slice_off(offsetof(PrepImage, b2[0]));
+  const uint64_t h1 = dimg + slice_off(offsetof(PrepImage, b2[1]));
+  const uint64_t l0 = dimg + slice_off(offsetof(PrepImage, b2[2]));
+  const uint64_t l1 = dimg + slice_off(offsetof(PrepImage, b2[3]));
+  const uint64_t bb = dimg + slice_off(offsetof(PrepImage, b2[4]));
+  tc::mma_ts(acc, op + 0, h0, idesc, 0);
+  tc::mma_ts(acc, op + 8, h1, idesc, 1);
+  tc::mma_ts(acc, op + 16, h0, idesc, 1);
+  tc::mma_ts(acc, op + 24, h1, idesc, 1);
+  tc::mma_ts(acc, op + 0, l0, idesc, 1);
+  tc::mma_ts(acc, op + 8, l1, idesc, 1);
+  tc::mma_ts(acc, one, bb, idesc, 1);
   tc::mma_commit(bar);
 }
 
@@ -333,8 +339,10 @@ __device__ __forceinline__ float max_nan_abs(float m, float x) {
 constexpr int kTraceTiles = 64;
 __device__ long long g_trace[kTraceTiles][8];
 __device__ __forceinline__ void trace(const DevicePlan &P, int32_t i, int ev) {
+#ifdef LOPT_TRACE
   if ((P.dbg & 32) && blockIdx.x == 0 && i < kTraceTiles && (threadIdx.x & 31) == 0)
     g_trace[i][ev] = clock64();
+#endif
 }
 
 // Ring position of a role: slot index and phase parity, advanced per tile.
@@ -367,15 +375,15 @@ __device__ __forceinline__ void wd_wait(uint64_t *bar, uint32_t parity, int tag,
 #define WAIT(bar, par, tag) tc::mbar_wait(bar, par)
 #endif
 
-// Ring position of a role that takes every kRoleWGs-th tile.
-template <int N>
+// Ring position of a role that takes every STEP-th tile.
+template <int N, int STEP>
 struct Stride {
   int i;
   uint32_t phase = 0;
   bool wrapped = false;
   __device__ __forceinline__ explicit Stride(int start) : i(start) {}
   __device__ __forceinline__ void next() {
-    i += kRoleWGs;
+    i += STEP;
     if (i >= N) {
       i -= N;
       phase ^= 1u;
@@ -402,7 +410,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       tc::mbar_init(&S.data_free[r], 4);
     }
     for (int b = 0; b < kImgs; b++) tc::mbar_init(&S.img_full[b], 1);
-    for (int w = 0; w < kRoleWGs; w++)
+    for (int w = 0; w < kWGsC; w++)
       for (int q = 0; q < 4; q++) S.c_done[w][q] = -1;
     for (int s = 0; s < kSlots; s++) {
       tc::mbar_init(&S.op_ready[s], 4);
@@ -432,7 +440,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
   const int32_t te = (int32_t)(P.n_tiles * (blockIdx.x + 1) / gridDim.x);
   const int32_t nt = aborted ? 0 : te - tb;
 
-  if (warp >= kWarpProducer && warp < kWarpProducer + kRoleWGs) {
+  if (warp >= kWarpProducer && warp < kWarpProducer + kProducers) {
     // -------------------------------------------------------------- producers
     // Producer p stages the tiles of parity p; both walk every tile so they
     // agree on the tensor sequence (image buffer k % kImgs for the k-th
@@ -456,13 +464,13 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
           const int32_t nf = nb == 0 ? first0 : nb == 1 ? first1 : nb == 2 ? first2 : first3;
           if (img == 0) first0 = i; else if (img == 1) first1 = i; else if (img == 2) first2 = i; else first3 = i;
           if (k >= kImgs) par_bits ^= 1u << img;
-          if ((i & 1) == p) {
+          if (i % kProducers == p) {
             if (k >= kImgs) {
               // tensor k - kImgs used tiles [pf, nf - 1]: every C warp must be
               // past the last tile of its parity in that range
               const int32_t last = nf - 1;
-              for (int w = 0; w < kRoleWGs; w++) {
-                const int32_t need = ((last & 1) == w) ? last : last - 1;
+              for (int w = 0; w < kWGsC; w++) {
+                const int32_t need = last - (((last - w) % kWGsC) + kWGsC) % kWGsC;
                 if (need < pf) continue;
                 for (int q = 0; q < 4; q++) {
                   int32_t d;
@@ -482,7 +490,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
                      (uint32_t)sizeof(PrepImage), &S.img_full[img]);
           }
         }
-        if ((i & 1) == p) {
+        if (i % kProducers == p) {
           if (rc.wrapped) WAIT(&S.data_free[rc.i], rc.phase ^ 1u, 1);
           trace(P, i, 0);
           pr.stage(S.stage[rc.i], &S.full[rc.i], img, (int)((par_bits >> img) & 1u), P.dbg);
@@ -496,18 +504,19 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     // --------------------------------------------------------------- MMA warps
     const bool l1 = warp == kWarpMma1;
     const uint32_t one = tbase + kOneCol;
+    const uint64_t dimg0 = tc::smem_desc_kmajor(tc::smem_u32(&S.img[0]), 512, 128);
     Cursor<kRing> rc;
     Cursor<kSlots> sc;
     for (int32_t i = 0; i < nt; i++) {
       WAIT(l1 ? &S.op_ready[sc.i] : &S.h_ready[sc.i], sc.phase, 4);
       tc::fence_after_sync();
       trace(P, i, l1 ? 3 : 5);
-      const PrepImage &im = S.img[S.stage[rc.i].meta.img];
+      const uint64_t dimg =
+          dimg0 + (uint64_t)((uint32_t)S.stage[rc.i].meta.img * (uint32_t)(sizeof(PrepImage) >> 4));
       const uint32_t op = tbase + 64 * sc.i, acc = op + 32;
       if (tc::elect_one()) {
-        if (P.dbg & 1) tc::mma_commit(l1 ? &S.acc1_full[sc.i] : &S.acc2_full[sc.i]);
-        else if (l1) issue_layer1(im, op, acc, &S.acc1_full[sc.i]);
-        else issue_layer2(im, op, acc, one, &S.acc2_full[sc.i]);
+        if (l1) issue_layer1(dimg, op, acc, &S.acc1_full[sc.i]);
+        else issue_layer2(dimg, op, acc, one, &S.acc2_full[sc.i]);
       }
       __syncwarp();
       rc.next();
@@ -516,13 +525,14 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
   } else if (warp < kWarpB) {
     // ------------------------------------------ WG_A: features -> E/B operands
     const int r0 = (warp - kWarpA) >> 2;
+    constexpr int kStep = kWGsA;
     const bool adv = P.state_advanced != 0;
     const float *beta = P.beta;
     int32_t col_j = -1, col_b0 = -1;   // rowblock: cached column entry of this lane
     Entry ce;
-    Stride<kRing> rc(r0);
-    Stride<kSlots> sc(r0);
-    for (int32_t i = r0; i < nt; i += kRoleWGs) {
+    Stride<kRing, kStep> rc(r0);
+    Stride<kSlots, kStep> sc(r0);
+    for (int32_t i = r0; i < nt; i += kStep) {
       WAIT(&S.full[rc.i], rc.phase, 5);
       if (warp == 0) trace(P, i, 1);
       const Stage &st = S.stage[rc.i];
@@ -610,9 +620,10 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
   } else if (warp < kWarpC) {
     // ------------------------------------------- WG_B: layer-1 epilogue -> H
     const int r0 = (warp - kWarpB) >> 2;
-    Stride<kRing> rc(r0);
-    Stride<kSlots> sc(r0);
-    for (int32_t i = r0; i < nt; i += kRoleWGs) {
+    constexpr int kStep = kWGsB;
+    Stride<kRing, kStep> rc(r0);
+    Stride<kSlots, kStep> sc(r0);
+    for (int32_t i = r0; i < nt; i += kStep) {
       WAIT(&S.full[rc.i], rc.phase, 5);
       const int img = S.stage[rc.i].meta.img;
       WAIT(&S.acc1_full[sc.i], sc.phase, 7);
@@ -654,14 +665,15 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
   } else if (warp < kWarpProducer) {
     // ------------------------- WG_C: layer-2 epilogue, layer 3, update, store
     const int r0 = (warp - kWarpC) >> 2;
+    constexpr int kStep = kWGsC;
     const float alpha_log2e = P.alpha * 1.4426950408889634f;
     const float dsb = P.step->ds * P.beta_out;
     const float decay = P.step->apply_decay != 0 ? P.step->decay : 1.0f;
     int red_j = -1;
     float red_max = 0.0f, red_out = 0.0f;   // max |delta|, NaN-propagating max |theta'|
-    Stride<kRing> rc(r0);
-    Stride<kSlots> sc(r0);
-    for (int32_t i = r0; i < nt; i += kRoleWGs) {
+    Stride<kRing, kStep> rc(r0);
+    Stride<kSlots, kStep> sc(r0);
+    for (int32_t i = r0; i < nt; i += kStep) {
       WAIT(&S.full[rc.i], rc.phase, 5);
       const Stage &st = S.stage[rc.i];
       const TileMeta &mt = st.meta;

@@ -78,6 +78,9 @@ __device__ __forceinline__ void advance(float g, float4 s, bool advanced, const 
   if (advanced) {
     x.m1 = s.x; x.m2 = s.y; x.m3 = s.z; x.v = s.w;
   } else {
+    // state.py:77-90 bit for bit: both products rounded, then the sum
+    // (packed f32x2 forms were measured to differ in the last bit: ptxas may
+    // contract them, so the advance stays scalar with explicit rounding)
     x.m1 = ema(beta[0], __fsub_rn(1.0f, beta[0]), s.x, g);
     x.m2 = ema(beta[1], __fsub_rn(1.0f, beta[1]), s.y, g);
     x.m3 = ema(beta[2], __fsub_rn(1.0f, beta[2]), s.z, g);
@@ -97,13 +100,20 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 __device__ __forceinline__ void fast_features(const FastIn &x, const float *rc, const float *cc,
                                               const float *sqmr, float *f) {
   const float svi = rsqrt_ftz(x.v + kEpsRecip);
-  float s[3];
-#pragma unroll
-  for (int i = 0; i < 3; i++) s[i] = sqmr[i] * rsqrt_ftz(fmaf(rc[i], cc[i], kEpsRecip));
+  const float2 rc01 = tc::fma2(make_float2(rc[0], rc[1]), make_float2(cc[0], cc[1]),
+                               make_float2(kEpsRecip, kEpsRecip));
+  const float rc2 = fmaf(rc[2], cc[2], kEpsRecip);
+  const float2 s01 = tc::mul2(make_float2(sqmr[0], sqmr[1]),
+                              make_float2(rsqrt_ftz(rc01.x), rsqrt_ftz(rc01.y)));
+  const float s2 = sqmr[2] * rsqrt_ftz(rc2);
+  const float2 m12 = make_float2(x.m1, x.m2);
+  const float2 a = tc::mul2(m12, make_float2(svi, svi));
+  const float2 b = tc::mul2(make_float2(x.g, x.g), s01);
+  const float2 c = tc::mul2(m12, s01);
   f[0] = x.m1; f[1] = x.m2; f[2] = x.m3; f[3] = x.v;
-  f[4] = x.m1 * svi; f[5] = x.m2 * svi; f[6] = x.m3 * svi; f[7] = svi;
-  f[8] = x.g * s[0]; f[9] = x.g * s[1]; f[10] = x.g * s[2];
-  f[11] = x.m1 * s[0]; f[12] = x.m2 * s[1]; f[13] = x.m3 * s[2];
+  f[4] = a.x; f[5] = a.y; f[6] = x.m3 * svi; f[7] = svi;
+  f[8] = b.x; f[9] = b.y; f[10] = x.g * s2;
+  f[11] = c.x; f[12] = c.y; f[13] = x.m3 * s2;
   f[14] = x.w; f[15] = x.g;
 }
 
