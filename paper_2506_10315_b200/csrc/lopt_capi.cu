@@ -26,6 +26,7 @@ int fast_supported(const DevicePlan &P);
 void launch_fast_stats(const DevicePlan &P, cudaStream_t s);
 void launch_fast_apply(const DevicePlan &P, cudaStream_t s);
 int64_t fast_stat_chunk();
+int64_t fast_stat_strip();
 int64_t fast_apply_chunk();
 size_t prep_image_bytes();
 int64_t factor_strip_cols();
@@ -172,8 +173,29 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
     rows += t.m;
     cols += t.n;
     d.stat_item0 = (int32_t)p->sitems.size();
-    for (int64_t e = t.lo; e < t.hi; e += stat_chunk)
-      p->sitems.push_back(ChunkItem{j, 0, e, std::min<int64_t>(t.hi, e + stat_chunk)});
+    auto flat_items = [&](int64_t e0, int64_t e1) {
+      for (int64_t e = e0; e < e1; e += stat_chunk)
+        p->sitems.push_back(ChunkItem{j, 0, e, std::min<int64_t>(e1, e + stat_chunk)});
+    };
+    const int64_t strip_w = fast_stat_strip();
+    if (fast && t.n % strip_w == 0 && t.hi > t.lo) {
+      // full rows as column strips (stat_chunk / strip_w rows x strip_w columns),
+      // a partial first / last row (element-range shards) as flat chunks
+      const int64_t a0 = (t.lo + t.n - 1) / t.n, a1 = t.hi / t.n;
+      if (a1 > a0) {
+        flat_items(t.lo, a0 * t.n);
+        const int64_t rows = std::max<int64_t>(1, stat_chunk / strip_w);
+        for (int64_t b = 0; b < t.n; b += strip_w)
+          for (int64_t a = a0; a < a1; a += rows)
+            p->sitems.push_back(ChunkItem{j, 1, (a << 32) | b,
+                                          (std::min<int64_t>(a1, a + rows) << 32) | (b + strip_w)});
+        flat_items(a1 * t.n, t.hi);
+      } else {
+        flat_items(t.lo, t.hi);
+      }
+    } else {
+      flat_items(t.lo, t.hi);
+    }
     d.stat_items = (int32_t)p->sitems.size() - d.stat_item0;
     d.apply_item0 = (int32_t)p->aitems.size();
     d.tile0 = p->n_tiles;

@@ -60,8 +60,11 @@ struct FactorItem {
 };
 
 // Phase-1/2 chunk: flat elements [e0, e1) of one tensor, e0 >= lo, e1 <= hi.
+// Fast-mode stats also use column strips (strip = 1): rows [e0 >> 32, e1 >> 32)
+// x columns [e0 & 0xffffffff, e1 & 0xffffffff) of a tensor whose rows in that
+// range lie entirely inside [lo, hi).
 struct ChunkItem {
-  int32_t tensor, pad_;
+  int32_t tensor, strip;
   int64_t e0, e1;
 };
 

@@ -145,80 +145,117 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
 }
 
 // Phase 1 (engine.py:619-654): per-element column sums of squares of the 16
-// (VeLO 17) per-element features; f32 per thread over its 32 elements, then a
-// fixed-order f64 block reduction.
+// (VeLO 17) per-element features; f32 per thread, then a fixed-order f64 block
+// reduction.  Four consecutive elements per thread per step with 16-byte loads
+// of theta and g; full groups run unmasked, only a chunk's ragged end is
+// masked, and the row-table entry is loaded once per group when the four
+// elements share a row.
 template <int KIND>
-__global__ void __launch_bounds__(kFastStatThreads) stats_fast_kernel(DevicePlan P) {
+__device__ __forceinline__ void stats_accum(float w, float g, float4 st, const float4 &rt,
+                                            const float4 &ct, bool adv, const float *beta,
+                                            const float *sqmr, float m, float *acc) {
+  constexpr int NE = KIND == LOPT_VELO_MLP ? 17 : 16;
+  FastIn x;
+  x.w = w;
+  advance(g, st, adv, beta, x);
+  const float rc[3] = {rt.x, rt.y, rt.z}, cc[3] = {ct.x, ct.y, ct.z};
+  float f[16];
+  fast_features(x, rc, cc, sqmr, f);
+  if (m != 1.0f) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) f[k] *= m;
+  }
+#pragma unroll
+  for (int k = 0; k < 16; k++) acc[k] = fmaf(f[k], f[k], acc[k]);
+  if (KIND == LOPT_VELO_MLP) {
+    const float cg = clip01(x.g) * m;
+    acc[NE - 1] = fmaf(cg, cg, acc[NE - 1]);
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kFastStatThreads, 4) stats_fast_kernel(DevicePlan P) {
   constexpr int D = d_feat(KIND);
   constexpr int NE = KIND == LOPT_VELO_MLP ? 17 : 16;
   const ChunkItem it = P.stat_items[blockIdx.x];
-  const TensorDesc T = P.tensors[it.tensor];
+  const TensorDesc &T = P.tensors[it.tensor];
+  const float *theta = T.theta, *grad = T.grad, *rowtab = T.rowtab, *coltab = T.coltab;
+  const float4 *state = T.state;
+  const int64_t n = T.n, lo = T.lo;
   const TensorScalars ts = P.tscal[it.tensor];
   const float sqmr[3] = {sqrtf(ts.mr[0]), sqrtf(ts.mr[1]), sqrtf(ts.mr[2])};
-  const double inv_n = 1.0 / (double)T.n;
-  __shared__ double red[kFastStatThreads / 32][NE];
+  const double inv_n = 1.0 / (double)n;
+  __shared__ float red[kFastStatThreads / 32][NE];
   float acc[NE];
 #pragma unroll
   for (int k = 0; k < NE; k++) acc[k] = 0.0f;
   const bool adv = P.state_advanced != 0;
-  // four consecutive elements per thread per step: 16-byte loads of theta and
-  // g when the chunk is aligned, one divmod per four elements
-  const bool vec = ((it.e0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(T.theta) & 15) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(T.grad) & 15) == 0);
-  for (int64_t e = it.e0 + 4 * threadIdx.x; e < it.e1; e += 4 * kFastStatThreads) {
-    const int cnt = it.e1 - e < 4 ? (int)(it.e1 - e) : 4;
-    float w4[4], g4[4];
-    if (vec && cnt == 4) {
-      const float4 w = __ldg(reinterpret_cast<const float4 *>(T.theta + e));
-      const float4 g = __ldg(reinterpret_cast<const float4 *>(T.grad + e));
-      w4[0] = w.x; w4[1] = w.y; w4[2] = w.z; w4[3] = w.w;
-      g4[0] = g.x; g4[1] = g.y; g4[2] = g.z; g4[3] = g.w;
-    } else {
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        w4[u] = u < cnt ? __ldg(T.theta + e + u) : 0.0f;
-        g4[u] = u < cnt ? __ldg(T.grad + e + u) : 0.0f;
-      }
+  if (it.strip) {
+    // column strip: this thread's column b for rows [ra, rb); its column
+    // entry is loaded once, the row entry is the same for the whole warp
+    const int64_t ra = it.e0 >> 32, rb = it.e1 >> 32;
+    const int64_t b = (it.e0 & 0xffffffffll) + threadIdx.x;
+    const float4 ct = __ldg(reinterpret_cast<const float4 *>(coltab + b * kRowTab));
+    const float *tp = theta + ra * n + b, *gp = grad + ra * n + b;
+    const float4 *sp = state + (ra * n + b - lo);
+#pragma unroll 2
+    for (int64_t a = ra; a < rb; a++) {
+      const float4 rt = __ldg(reinterpret_cast<const float4 *>(rowtab + a * kRowTab));
+      stats_accum<KIND>(__ldg(tp), __ldg(gp), __ldg(sp), rt, ct, adv, P.beta, sqmr, 1.0f, acc);
+      tp += n;
+      gp += n;
+      sp += n;
     }
-    // every load of the four elements is issued before any arithmetic
-    float4 s4[4], rt[4], ct[4];
+  } else {
+  const bool vec = ((it.e0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(theta) & 7) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(grad) & 7) == 0);
+  // two consecutive elements per thread per step (64 registers: four CTAs
+  // per SM keep enough loads in flight to cover HBM latency)
+  int64_t e = it.e0 + 2 * threadIdx.x;
+  for (; e < it.e1; e += 2 * kFastStatThreads) {
+    const int cnt = it.e1 - e < 2 ? (int)(it.e1 - e) : 2;
     int64_t a, b;
-    divmod(e, T.n, inv_n, a, b);
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const bool ok = u < cnt;
-      s4[u] = __ldg(T.state + (ok ? e + u - T.lo : e - T.lo));
-      rt[u] = __ldg(reinterpret_cast<const float4 *>(T.rowtab + a * kRowTab));
-      ct[u] = __ldg(reinterpret_cast<const float4 *>(T.coltab + b * kRowTab));
-      if (++b >= T.n) {
-        b = 0;
-        a = a + 1 < T.m ? a + 1 : a;
+    divmod(e, n, inv_n, a, b);
+    if (cnt == 2 && vec) {
+      const float2 w2 = __ldg(reinterpret_cast<const float2 *>(theta + e));
+      const float2 g2 = __ldg(reinterpret_cast<const float2 *>(grad + e));
+      const float4 *sp = state + (e - lo);
+      const float4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
+      const float4 r0 = __ldg(reinterpret_cast<const float4 *>(rowtab + a * kRowTab));
+      const float4 c0 = __ldg(reinterpret_cast<const float4 *>(coltab + b * kRowTab));
+      float4 r1 = r0, c1;
+      if (b + 1 < n) {
+        c1 = __ldg(reinterpret_cast<const float4 *>(coltab + (b + 1) * kRowTab));
+      } else {
+        r1 = __ldg(reinterpret_cast<const float4 *>(rowtab + (a + 1) * kRowTab));
+        c1 = __ldg(reinterpret_cast<const float4 *>(coltab));
       }
-    }
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const float m = u < cnt ? 1.0f : 0.0f;   // masked lanes add zeros
-      FastIn x;
-      x.w = w4[u];
-      advance(g4[u], s4[u], adv, P.beta, x);
-      const float rc[3] = {rt[u].x, rt[u].y, rt[u].z}, cc[3] = {ct[u].x, ct[u].y, ct[u].z};
-      float f[16];
-      fast_features(x, rc, cc, sqmr, f);
-#pragma unroll
-      for (int k = 0; k < 16; k++) {
-        const float fm = f[k] * m;
-        acc[k] = fmaf(fm, fm, acc[k]);
-      }
-      if (KIND == LOPT_VELO_MLP) {
-        const float cg = clip01(x.g) * m;
-        acc[NE - 1] = fmaf(cg, cg, acc[NE - 1]);
+      stats_accum<KIND>(w2.x, g2.x, s0, r0, c0, adv, P.beta, sqmr, 1.0f, acc);
+      stats_accum<KIND>(w2.y, g2.y, s1, r1, c1, adv, P.beta, sqmr, 1.0f, acc);
+    } else {
+      // ragged or unaligned pair: element by element, masked
+      int64_t aa = a, bb = b;
+      for (int u = 0; u < 2; u++) {
+        const bool ok = u < cnt;
+        const int64_t eu = ok ? e + u : e;
+        const float4 rt = __ldg(reinterpret_cast<const float4 *>(rowtab + aa * kRowTab));
+        const float4 ct = __ldg(reinterpret_cast<const float4 *>(coltab + bb * kRowTab));
+        stats_accum<KIND>(__ldg(theta + eu), __ldg(grad + eu), __ldg(state + (eu - lo)), rt, ct,
+                          adv, P.beta, sqmr, ok ? 1.0f : 0.0f, acc);
+        if (++bb >= n) {
+          bb = 0;
+          aa = aa + 1 < T.m ? aa + 1 : aa;
+        }
       }
     }
   }
+  }
+  // warp reduction in f32 (each lane holds at most 32 elements' worth), then
+  // a fixed-order f64 block reduction
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < NE; k++) {
-    const double s = warp_sum((double)acc[k]);
+    const float s = warp_sum(acc[k]);
     if (lane == 0) red[warp][k] = s;
   }
   __syncthreads();
@@ -226,13 +263,13 @@ __global__ void __launch_bounds__(kFastStatThreads) stats_fast_kernel(DevicePlan
   for (int c = threadIdx.x; c < D; c += blockDim.x) {
     // reference column c <- per-element slot, or 0 for broadcast/time columns
     int q = -1;
-    for (int s = 0; s < 16; s++)
-      if (elem_col(KIND, s) == c) q = s;
+    for (int s2 = 0; s2 < 16; s2++)
+      if (elem_col(KIND, s2) == c) q = s2;
     if (KIND == LOPT_VELO_MLP && c == 28) q = 16;
     double v = 0.0;
     if (q >= 0) {
 #pragma unroll
-      for (int w = 0; w < kFastStatThreads / 32; w++) v += red[w][q];
+      for (int w = 0; w < kFastStatThreads / 32; w++) v += (double)red[w][q];
     }
     out[c] = v;
   }
@@ -264,6 +301,7 @@ int fast_supported(const DevicePlan &P) {
   return P.h1 == 32 && P.h2 == 32 && P.n_tiles < ((int64_t)1 << 31) ? 1 : 0;
 }
 int64_t fast_stat_chunk() { return kFastStatChunk; }
+int64_t fast_stat_strip() { return kFastStatThreads; }
 int64_t fast_apply_chunk() { return kTile; }
 size_t prep_image_bytes() { return sizeof(PrepImage); }
 
