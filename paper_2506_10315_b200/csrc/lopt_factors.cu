@@ -7,6 +7,8 @@
 // turn them into per-row / per-column f64 sums, which is also the block a
 // multi-GPU caller all-reduces (distsim.py:448-474).  No float atomics: the
 // result is bit-reproducible for a fixed plan.
+#include <algorithm>
+
 #include "lopt_common.cuh"
 #include "lopt_tc.cuh"
 
@@ -77,7 +79,7 @@ __device__ void factor_tile(const DevicePlan &P, const FactorItem &it, const Ten
       if (r == 1 && !has2) break;
       const int64_t row = r == 0 ? a : a2;
       const bool full = row * n >= T.lo && (row + 1) * n <= T.hi;
-      double rowp = 0.0;
+      double rowp2[2] = {0.0, 0.0};   // two chains: half the dependent DADD latency
 #pragma unroll
       for (int k = 0; k < 16; k++) {
         double sq = (double)v[r][k] * (double)v[r][k];
@@ -86,9 +88,9 @@ __device__ void factor_tile(const DevicePlan &P, const FactorItem &it, const Ten
           if (e < T.lo || e >= T.hi) sq = 0.0;
         }
         colacc[k] += sq;
-        rowp += sq;
+        rowp2[k & 1] += sq;
       }
-      rowp = warp_sum(rowp);
+      double rowp = warp_sum(rowp2[0] + rowp2[1]);
       if (lane == 0) {
         T.rowpart[(int64_t)it.strip * T.m + row] = rowp;
         bad |= !isfinite(rowp);
@@ -152,15 +154,19 @@ __device__ void factor_vector(const DevicePlan &P, const FactorItem &it, const T
   }
 }
 
+// One CTA per item (the loop also allows a persistent launch).
 __global__ void __launch_bounds__(kFactorThreads, 2) factor_partials_kernel(DevicePlan P) {
-  const FactorItem it = P.factor_items[blockIdx.x];
-  const TensorDesc T = P.tensors[it.tensor];
-  if (T.n == 1) {
-    factor_vector(P, it, T);
-  } else if ((T.n & 3) == 0 && (reinterpret_cast<uintptr_t>(T.grad) & 15) == 0) {
-    factor_tile<true>(P, it, T);
-  } else {
-    factor_tile<false>(P, it, T);
+  for (int item = blockIdx.x; item < P.n_factor_items; item += gridDim.x) {
+    const FactorItem it = P.factor_items[item];
+    const TensorDesc T = P.tensors[it.tensor];
+    if (T.n == 1) {
+      factor_vector(P, it, T);
+    } else if ((T.n & 3) == 0 && (reinterpret_cast<uintptr_t>(T.grad) & 15) == 0) {
+      factor_tile<true>(P, it, T);
+    } else {
+      factor_tile<false>(P, it, T);
+    }
+    __syncthreads();   // shared scratch is reused by the next item
   }
 }
 
@@ -291,7 +297,18 @@ __global__ void __launch_bounds__(256) factor_means_kernel(DevicePlan P) {
 
 int64_t factor_strip_cols() { return kStripCols; }
 
+static int g_factor_sms = 0;
+
 void launch_factor_partials(const DevicePlan &P, cudaStream_t s) {
+  if (g_factor_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_factor_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_factor_sms <= 0) g_factor_sms = 148;
+  }
+  // one CTA per item (measured faster than a persistent grid: items differ in
+  // size, and short CTAs backfill)
+  (void)g_factor_sms;
   if (P.n_factor_items > 0) factor_partials_kernel<<<P.n_factor_items, kFactorThreads, 0, s>>>(P);
 }
 
