@@ -45,9 +45,12 @@ def worker_ranges(lo: int, hi: int, workers: int):
 def flat_shard_ranges(sizes, world: int, rank: int):
     """Per-tensor local ranges of rank `rank` when the concatenation of the
     tensors (in order) is cut into `world` equal contiguous slices (the arena
-    is padded to a multiple of `world`).  Returns (ranges, slice_len, padded)."""
+    is padded to a multiple of 128 * `world`).  Returns (ranges, slice_len, padded)."""
     total = int(sum(sizes))
-    padded = (total + world - 1) // world * world
+    # slices are whole multiples of 128 elements, so shard boundaries fall on
+    # tile boundaries of the fast path (16-byte aligned bulk copies)
+    unit = world * 128
+    padded = (total + unit - 1) // unit * unit
     S = padded // world
     s0, s1 = rank * S, (rank + 1) * S
     out, off = [], 0
