@@ -49,7 +49,7 @@ constexpr int kApplyThreads = (kWGsA + kWGsB + kWGsC) * 128 + (kProducers + 2) *
 constexpr int kWarpA = 0, kWarpB = 4 * kWGsA, kWarpC = kWarpB + 4 * kWGsB;
 constexpr int kWarpProducer = kWarpC + 4 * kWGsC;
 constexpr int kWarpMma1 = kWarpProducer + kProducers, kWarpMma2 = kWarpMma1 + 1;
-static_assert(kRing % kProducers == 0 && kRing % kWGsA == 0 && kRing % kWGsC == 0, "ring ownership");
+static_assert(kWGsA < kSlots && kWGsC < kSlots && kProducers < kRing, "cursor strides");
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kOneCol = 64 * kSlots;   // shared constant slice
 static_assert(kOneCol + 8 <= kTmemCols, "TMEM budget");
