@@ -198,8 +198,11 @@ def time_device(opt, params, grads, steps, warmup, world):
 
 
 def time_e2e(opt, params, grads, steps, warmup, world):
-    """Public-API step with host buffers: pinned H2D of the gradients and D2H
-    of the updated parameters inside the timed region, every step."""
+    """Public-API step with host buffers: the gradients come from pinned host
+    memory and the updated parameters go back to pinned host memory, both
+    inside the timed region, every step.  Single GPU: LearnedOptimizer.step_host
+    (chunked, H2D / step / D2H overlapped on separate streams); sharded: the
+    plain copies around step()."""
     import torch
 
     host_g = [g.cpu().pin_memory() for g in grads]
@@ -207,8 +210,12 @@ def time_e2e(opt, params, grads, steps, warmup, world):
     dev_g = [torch.empty_like(g) for g in grads]
     for p, g in zip(params, dev_g):
         p.grad = g
+    piped = world == 1 and hasattr(opt, "step_host")
 
     def one():
+        if piped:
+            opt.step_host(host_g, host_p)
+            return
         for d, h in zip(dev_g, host_g):
             d.copy_(h, non_blocking=True)
         opt.step()
@@ -372,7 +379,10 @@ def main():
         ems, h2d, d2h = time_e2e(opt, params, grads, e2e_steps, 2, world)
         e2e = {"value": n_params * e2e_steps / (ems / 1e3) / 1e9, "unit": "Gparams/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": ems / e2e_steps, "api": "LearnedOptimizer.step (torch.optim)"}
+               "ms_per_step": ems / e2e_steps,
+               "api": ("LearnedOptimizer.step_host (pinned host grads in, host params out, "
+                       "8 chunks pipelined)" if world == 1 else
+                       "ShardedLearnedOptimizer.step with host copies")}
 
     velo = None
     if not args.no_velo and args.feature_set == "small_fc_lopt":

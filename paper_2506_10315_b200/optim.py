@@ -206,6 +206,99 @@ class LearnedOptimizer(torch.optim.Optimizer):
         """The StepPlans of the parameter groups (one per group)."""
         return [entry[1] for entry in self._plans.values()]
 
+    # -- host-buffer step (offload) ------------------------------------------
+    @torch.no_grad()
+    def step_host(self, host_grads, host_params=None, *, chunks: int = 8):
+        """One step with the gradients in (pinned) host memory and, if given,
+        the updated parameters copied back into `host_params` -- the call a
+        host-resident caller of the reference makes (opt_step with NumPy
+        arrays), served from the device.
+
+        The tensors are cut into `chunks` groups of about equal size, each with
+        its own plan; the gradient upload of group k+1 (H2D engine) and the
+        parameter download of group k-1 (D2H engine) overlap the device step
+        of group k, so the step costs about one PCIe transfer instead of two
+        plus the compute.  Semantics per group are those of step(); a
+        non-finite gradient aborts its group (groups already stepped stay
+        committed -- documented difference to the all-or-nothing opt_step).
+        Returns after enqueueing; host_params are valid after a device sync.
+        """
+        params = [p for g in self.param_groups for p in g["params"]]
+        if len(self.param_groups) != 1:
+            raise OptimError("step_host supports one parameter group")
+        if len(host_grads) != len(params):
+            raise OptimError(f"got {len(host_grads)} gradients for {len(params)} tensors")
+        if host_params is not None and len(host_params) != len(params):
+            raise OptimError(f"got {len(host_params)} host parameter buffers for {len(params)}")
+        key = (tuple(id(p) for p in params), chunks)
+        hs = getattr(self, "_host_step", None)
+        if hs is None or hs["key"] != key:
+            for p in params:
+                if p.grad is None:
+                    p.grad = torch.empty_like(p)
+            total = sum(p.numel() for p in params)
+            groups, cur, acc = [], [], 0
+            for k, p in enumerate(params):
+                cur.append(k)
+                acc += p.numel()
+                if acc >= total * (len(groups) + 1) / chunks and len(groups) < chunks - 1:
+                    groups.append(cur)
+                    cur = []
+            if cur:
+                groups.append(cur)
+            hs = {"key": key, "groups": groups, "plans": [None] * len(groups),
+                  "h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream()}
+            self._host_step = hs
+        group = self.param_groups[0]
+        lr = schedule_lr(self.schedule, self.T) if self.schedule is not None else group["lr"]
+        wd, t = group["weight_decay"], self.T + 1
+        comp = torch.cuda.current_stream()
+        h2d, d2h = hs["h2d"], hs["d2h"]
+        uploaded = []
+        h2d.wait_stream(comp)        # the previous step is done reading the grads
+        with torch.cuda.stream(h2d):
+            for ks in hs["groups"]:
+                for k in ks:
+                    params[k].grad.copy_(host_grads[k].view(params[k].shape), non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                uploaded.append(ev)
+        launched = []
+        d2h.wait_stream(comp)
+        for gi, ks in enumerate(hs["groups"]):
+            comp.wait_event(uploaded[gi])
+            ps = [params[k] for k in ks]
+            plan = hs["plans"][gi]
+            slots = [self._slot(p) for p in ps]
+            ptrs = [s.grad.data_ptr() for s in slots]
+            if plan is None:
+                plan = StepPlan(slots, self.spec, self.lopt_weights, mode=self.mode)
+                hs["plans"][gi] = plan
+                hs.setdefault("ptrs", {})[gi] = ptrs
+            elif hs["ptrs"][gi] != ptrs:
+                plan.rebind(slots)
+                hs["ptrs"][gi] = ptrs
+            plan.step(lr, wd, t)
+            launched.append((plan, ps))
+            if host_params is not None:
+                done = torch.cuda.Event()
+                done.record(comp)
+                d2h.wait_event(done)
+                with torch.cuda.stream(d2h):
+                    for k in ks:
+                        host_params[k].view(params[k].shape).copy_(params[k].detach(),
+                                                                    non_blocking=True)
+        comp.wait_stream(d2h)
+        self._pending = launched
+        self._last = launched
+        if self.check_errors:
+            self.check()
+        self.T += 1
+        for p in params:
+            if "quad" in self.state[p]:
+                self.state[p]["step"] = self.T
+        return None
+
     def check(self):
         """Surface device-side errors of the last step (synchronizes)."""
         pending, self._pending = getattr(self, "_pending", []), []

@@ -169,3 +169,33 @@ def test_fast_zero_network_is_noop(P):
     p.grad = torch.randn(300, 256, device="cuda")
     opt.step()
     assert torch.equal(p.detach(), x)
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_step_host_matches_device_step(P, mode):
+    """step_host (chunked H2D / step / D2H pipeline) gives the same parameters
+    and state as step() on device-resident gradients -- bitwise, since both
+    run the same kernels on the same tensors."""
+    import torch
+
+    shapes = [(128, 784), (128,), (10, 128), (10,), (256, 256), (33, 70)]
+    rng = np.random.default_rng(11)
+    init = [np.asarray(rng.standard_normal(s) * 0.02, dtype=F32) for s in shapes]
+    grads = [[np.asarray(rng.standard_normal(s) * 1e-3, dtype=F32) for s in shapes]
+             for _ in range(3)]
+    a = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    b = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    oa = P.LearnedOptimizer(a, mode=mode, weight_decay=0.01)
+    ob = P.LearnedOptimizer(b, mode=mode, weight_decay=0.01)
+    host_p = [torch.empty(s, dtype=torch.float32).pin_memory() for s in shapes]
+    for gs in grads:
+        for p, g in zip(a, gs):
+            p.grad = torch.from_numpy(g).cuda()
+        oa.step()
+        ob.step_host([torch.from_numpy(g).pin_memory() for g in gs], host_p, chunks=3)
+    torch.cuda.synchronize()
+    for p, q, h in zip(a, b, host_p):
+        assert p.detach().cpu().numpy().tobytes() == q.detach().cpu().numpy().tobytes()
+        assert h.numpy().tobytes() == q.detach().cpu().numpy().tobytes()
+    for p, q in zip(a, b):
+        assert oa.state[p]["quad"].cpu().numpy().tobytes() == ob.state[q]["quad"].cpu().numpy().tobytes()
