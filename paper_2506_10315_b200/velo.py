@@ -91,7 +91,19 @@ class _VeLOMixin:
             raise OptimError("VeLO needs the loss: call optimizer.step(loss) (PAPER.md:600)")
         lv = math.log(max(float(loss), 1e-8))
         self._loss_ema = lv if self._loss_ema is None else 0.9 * self._loss_ema + 0.1 * lv
-        self._loss_dev.copy_(torch.tensor([lv, self._loss_ema], dtype=torch.float32))
+        # stream-ordered upload from a small ring of pinned buffers (a pageable
+        # copy would stall the host on every step)
+        ring = getattr(self, "_loss_ring", None)
+        if ring is None:
+            ring = self._loss_ring = [(torch.empty(2, dtype=torch.float32).pin_memory(),
+                                       torch.cuda.Event()) for _ in range(4)]
+            self._loss_k = 0
+        buf, ev = ring[self._loss_k % len(ring)]
+        self._loss_k += 1
+        ev.synchronize()   # the copy that last used this buffer has finished
+        buf[0], buf[1] = lv, self._loss_ema
+        self._loss_dev.copy_(buf, non_blocking=True)
+        ev.record()
 
     def _after_stats(self, gi, plan, params):
         st = self._lstm_state(gi, params)
