@@ -54,7 +54,9 @@ constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kOneCol = 64 * kSlots;   // shared constant slice
 static_assert(kOneCol + 8 <= kTmemCols, "TMEM budget");
 
-constexpr int32_t kFlagRowblock = 1, kFlagSlow = 2;
+// kFlagTail: one of the last kWGsC tiles of its tensor -- the C warps publish
+// their progress there (image-buffer reuse), nowhere else
+constexpr int32_t kFlagRowblock = 1, kFlagSlow = 2, kFlagTail = 4;
 
 // Written by the producer for every tile it stages.  Lane pointers are
 // pre-offset to the tile's first element, so lane i uses ptr + i.
@@ -245,7 +247,7 @@ struct Producer {
     mt.v0 = v0;
     mt.v1 = v1;
     const bool fast = aligned && ((el0 + v0) & 3) == 0 && ((v1 - v0) & 3) == 0;
-    mt.flags = (rb ? kFlagRowblock : 0) | (fast ? 0 : kFlagSlow);
+    mt.flags = (rb ? kFlagRowblock : 0) | (fast ? 0 : kFlagSlow) | (left <= kWGsC ? kFlagTail : 0);
     mt.img = img;
     mt.img_par = img_par;
     mt.pad0[0] = mt.pad0[1] = mt.pad0[2] = 0;
@@ -529,6 +531,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     const bool adv = P.state_advanced != 0;
     const float *beta = P.beta;
     int32_t col_j = -1, col_b0 = -1;   // rowblock: cached column entry of this lane
+    int32_t a_img = -1, a_par = -1;    // operand image last waited for
     Entry ce;
     Stride<kRing, kStep> rc(r0);
     Stride<kSlots, kStep> sc(r0);
@@ -539,7 +542,11 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       const TileMeta &mt = st.meta;
       const int32_t flags = mt.flags;
       const bool valid = row >= mt.v0 && row < mt.v1;
-      WAIT(&S.img_full[mt.img], (uint32_t)mt.img_par, 9);
+      if (mt.img != a_img || mt.img_par != a_par) {   // a new operand image: wait for its load
+        WAIT(&S.img_full[mt.img], (uint32_t)mt.img_par, 9);
+        a_img = mt.img;
+        a_par = mt.img_par;
+      }
       const PrepImage &im = S.img[mt.img];
       float4 *sp = mt.state + row;
       float w, g;
@@ -678,6 +685,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       const Stage &st = S.stage[rc.i];
       const TileMeta &mt = st.meta;
       const int j = mt.j;
+      const int32_t mt_flags = mt.flags;
       if (j != red_j) {
         if (red_j >= 0) {
           if (red_max > 0.0f)
@@ -723,7 +731,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       }
       // the data slot (theta, meta) and the image are no longer needed
       warp_arrive(&S.data_free[rc.i]);
-      if ((threadIdx.x & 31) == 0)
+      if ((mt_flags & kFlagTail) && (threadIdx.x & 31) == 0)
         asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&S.c_done[r0][warp & 3])),
                      "r"(i)
                      : "memory");
