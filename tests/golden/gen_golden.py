@@ -6,7 +6,8 @@ Run in the build container (the reference is mounted read-only at
     PYTHONDONTWRITEBYTECODE=1 NUMBA_CACHE_DIR=/tmp/numba_cache \
         python tests/golden/gen_golden.py
 
-Outputs tests/golden/*.npz.  Every array in them is produced by the
+Outputs tests/golden/*.npz and the reference-written PYLO files
+tests/golden/ref_*.pylo (container / checkpoint interop).  Every array in them is produced by the
 reference's own public functions (pkg/src/lopt/...), on inputs generated here
 from fixed seeds.  tests/test_oracle_golden.py checks the C oracle against
 these files bit for bit; the GPU parity tests then check the CUDA path
@@ -148,14 +149,61 @@ def state_cases(state_mod, features):
     return out
 
 
+def ckpt_cases(engine, features, optim, state_mod):
+    """Reference-written PYLO files (weights + checkpoints after 3 steps) and
+    the reference's continuation for 2 more steps from each checkpoint."""
+    from lopt import tensors
+
+    out = {}
+    runs = {
+        "small_const": dict(spec="small_fc_lopt", sched=optim.ScheduleConfig(kind="constant", max_lr=0.7),
+                            wd=0.0, wseed=3),
+        "velo_cos_wd": dict(spec="velo_mlp",
+                            sched=optim.ScheduleConfig(kind="cosine", max_lr=0.8, min_lr=0.05,
+                                                       warmup_steps=2, total_steps=8),
+                            wd=0.01, wseed=4),
+    }
+    for name, cfg in runs.items():
+        spec = features.spec_by_name(cfg["spec"])
+        rng = np.random.default_rng(91)
+        named = [(f"layer{i}", (rng.standard_normal(s) * 0.05).astype(F32))
+                 for i, s in enumerate(MODEL_SHAPES)]
+        w = engine.random_weights(spec.d_feat, seed=cfg["wseed"])
+        engine.save_weights(w, spec, os.path.join(OUT, f"ref_weights_{name}.pylo"))
+        h = optim.OptimizerHandle.fresh(named, w, spec, schedule=cfg["sched"], weight_decay=cfg["wd"])
+        grng = np.random.default_rng(92)
+        for step in range(5):
+            if step == 3:
+                optim.checkpoint_save(h, os.path.join(OUT, f"ref_ckpt_{name}.pylo"))
+            grads = [(grng.standard_normal(p.shape) * 1e-2).astype(F32) for _, p in h.params]
+            optim.opt_step(h, grads)
+            if step >= 3:
+                for j, g in enumerate(grads):
+                    out[f"{name}/step{step}/grad{j}"] = g
+                for j, (_, p) in enumerate(h.params):
+                    out[f"{name}/step{step}/param{j}"] = p.data
+        for j, s in enumerate(h.states):
+            out[f"{name}/final/state{j}/V"] = s.V
+            out[f"{name}/final/state{j}/M2"] = s.M[2]
+            out[f"{name}/final/state{j}/r1"] = s.r[1]
+    # a container with every dtype and a 0-d and an empty array, for the
+    # byte-for-byte writer comparison
+    tensors.file_save({"a": np.arange(6, dtype=F32).reshape(2, 3), "b": np.array(3.5),
+                       "c": np.arange(5, dtype=np.int64), "d": np.zeros((0, 4), F32)},
+                      {"kind": "misc", "note": "unicode \u00e9"}, os.path.join(OUT, "ref_misc.pylo"))
+    return out
+
+
 def main():
     engine, features, optim, state_mod = _import_reference()
+    np.savez_compressed(os.path.join(OUT, "ckpt_cases.npz"),
+                        **ckpt_cases(engine, features, optim, state_mod))
     np.savez_compressed(os.path.join(OUT, "engine_cases.npz"), **engine_cases(engine, features, state_mod))
     np.savez_compressed(os.path.join(OUT, "optstep_cases.npz"),
                         **optstep_cases(engine, features, optim, state_mod))
     np.savez_compressed(os.path.join(OUT, "state_cases.npz"), **state_cases(state_mod, features))
     for f in sorted(os.listdir(OUT)):
-        if f.endswith(".npz"):
+        if f.endswith((".npz", ".pylo")):
             print(f, os.path.getsize(os.path.join(OUT, f)))
 
 
