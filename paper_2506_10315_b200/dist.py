@@ -107,6 +107,44 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
             st["step"] = self.T
             st["range"] = (lo, hi)
 
+    # -- gradient reduce-scatter (all-reduce = reduce-scatter +
+    # all-gather; the step only needs this rank's slice of the summed
+    # gradient, and the all-gather is the parameter gather that follows) -----
+    def flat_grads(self) -> torch.Tensor:
+        """The gradient arena: p.grad of every parameter becomes a view of it,
+        laid out like the parameter arena (rank r's slice is its element
+        range).  Backward accumulates local (unreduced) gradients into it."""
+        if getattr(self, "_flat_grad", None) is None:
+            ps = self.param_groups[0]["params"]
+            self._flat_grad = torch.zeros_like(self.flat)
+            off = 0
+            for p in ps:
+                n = p.numel()
+                if p.grad is not None:
+                    self._flat_grad[off:off + n].copy_(p.grad.reshape(-1))
+                p.grad = self._flat_grad[off:off + n].view(p.shape)
+                off += n
+        return self._flat_grad
+
+    def reduce_scatter_grads(self, average: bool = True):
+        """Sum (or average) the ranks' local gradients so that each rank holds
+        the reduced values of its own slice -- all the sharded step reads
+        (distsim.py:323-334 mean_grads, restricted to the owned range).  One
+        in-place NCCL reduce-scatter: half the bytes of the all-reduce DDP
+        would otherwise run."""
+        fg = self.flat_grads()
+        S = self.slice_len
+        local = fg[self.rank * S:(self.rank + 1) * S]
+        if self._nccl():
+            dist.reduce_scatter_tensor(local, fg, group=self.pg)
+        else:   # gloo has no reduce-scatter: all-reduce through the host, keep the slice
+            h = fg.cpu()
+            dist.all_reduce(h, group=self.pg)
+            local.copy_(h[self.rank * S:(self.rank + 1) * S].to(fg.device))
+        if average:
+            local.div_(self.world)
+        return local
+
     def _slot(self, p, weight_slot=0) -> Slot:
         s = super()._slot(p, weight_slot)
         s.lo, s.hi = self.state[p]["range"]

@@ -157,3 +157,59 @@ def test_flat_shard_ranges_partition():
     assert max(b - a for a, b in r) - min(b - a for a, b in r) <= 1
     owners = owner_plan([5, 100, 7, 60, 60], 2)
     assert owners[1] == 0 and sorted(set(owners)) == [0, 1]
+
+
+def _rs_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_10315_b200.dist import ShardedLearnedOptimizer
+
+        rng = np.random.default_rng(0)
+        params = [torch.nn.Parameter(torch.from_numpy((rng.standard_normal(s) * 0.05).astype(F32)))
+                  for s in SHAPES]
+        opt = ShardedLearnedOptimizer(params)
+        # rank-dependent local gradients, accumulated into the gradient arena
+        lrng = np.random.default_rng(100 + rank)
+        fg = opt.flat_grads()
+        local_g = [(lrng.standard_normal(s) * 1e-2).astype(F32) for s in SHAPES]
+        for p, g in zip(params, local_g):
+            p.grad.copy_(torch.from_numpy(g))
+        sl = opt.reduce_scatter_grads(average=True).clone()
+        q.put((rank, opt.slice_len, [g.reshape(-1) for g in local_g], sl.numpy()))
+    except Exception:
+        import traceback
+        q.put((rank, -1, traceback.format_exc(), None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reduce_scatter_grads_gloo_world2():
+    """Each rank ends up with the mean of all ranks' gradients on exactly its
+    own slice of the flat arena (what the sharded step reads)."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rs_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in procs], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert r[1] > 0, r[2]
+    S = res[0][1]
+    flat = [np.concatenate(r[2]) for r in res]
+    mean = (flat[0] + flat[1]) / np.float32(2)
+    mean = np.concatenate([mean, np.zeros(2 * S - mean.size, np.float32)])
+    for rank, _, _, sl in res:
+        np.testing.assert_allclose(sl, mean[rank * S:(rank + 1) * S], rtol=0, atol=1e-9)
