@@ -628,16 +628,12 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     // ------------------------------------------- WG_B: layer-1 epilogue -> H
     const int r0 = (warp - kWarpB) >> 2;
     constexpr int kStep = kWGsB;
-    Stride<kRing, kStep> rc(r0);
     Stride<kSlots, kStep> sc(r0);
     for (int32_t i = r0; i < nt; i += kStep) {
-      WAIT(&S.full[rc.i], rc.phase, 5);
-      const int img = S.stage[rc.i].meta.img;
+      // B touches neither the data ring nor the operand image (the layer-1
+      // scale 2^-s2 is folded into W1): it waits for the accumulator only
       WAIT(&S.acc1_full[sc.i], sc.phase, 7);
       tc::fence_after_sync();
-      // the image is read only after acc1_full: A waited for its load before
-      // the MMAs of this tile were issued
-      const float sdown = S.img[img].s2_down;
       if (warp == kWarpB) trace(P, i, 4);
       const uint32_t ta = tbase + lane_addr + 64 * sc.i;
 #pragma unroll
@@ -649,10 +645,6 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
         } else {
           tc::tmem_ld16(ta + 32 + 16 * half, h);
           tc::tmem_ld_wait();
-        }
-        if (sdown != 1.0f) {
-#pragma unroll
-          for (int q = 0; q < 16; q++) h[q] = __float_as_uint(__uint_as_float(h[q]) * sdown);
         }
         uint32_t hi[8], lo[8];
 #pragma unroll
@@ -666,7 +658,6 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       tc::tmem_st_wait();
       tc::fence_before_sync();
       warp_arrive(&S.h_ready[sc.i]);
-      rc.next();
       sc.next();
     }
   } else if (warp < kWarpProducer) {

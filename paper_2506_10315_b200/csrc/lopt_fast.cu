@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
       v = bias1[o];                                          // the constant-1 column
     }
     uint16_t hi, lo;
-    split1(v, hi, lo);
+    split1(v * s2s[0], hi, lo);   // 2^-s2 folded into layer 1 (exact power of two)
     img->b1[2 * s][bslot(o, q)] = hi;
     img->b1[2 * s + 1][bslot(o, q)] = lo;
   }

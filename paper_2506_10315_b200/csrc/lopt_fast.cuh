@@ -23,8 +23,9 @@ constexpr int kTile = 128;
 // features x*scale (|x*scale| <= sqrt(m*n) < 65504 because
 // sum_e (x*scale)^2 <= m*n), so W1 is used unscaled.  Layer 2 takes
 // ReLU(h1) * 2^-s2 with s2 chosen per tensor from a bound on |h1| (s2 = 0 on
-// every tensor of the benchmarked models); the layer-2 bias is pre-scaled by
-// 2^-s2 and 2^s2 is folded into W3.
+// every tensor of the benchmarked models): 2^-s2 is folded into W1 and the
+// layer-1 bias (so the MMA emits h1 * 2^-s2), the layer-2 bias is pre-scaled
+// by 2^-s2 and 2^s2 is folded into W3.
 //
 // A operands (per 128-element tile, TMEM, 2 fp16 per 32-bit column):
 //   E_hi/E_lo  16 per-element features in elem_col order
@@ -39,7 +40,7 @@ struct __align__(128) PrepImage {
   float escale[20];         // normalization scale of the per-element columns (+ clip), float4-read
   float b3[2];
   float sqmr[3];            // sqrt(mean r_i)
-  float s2_down;            // 2^-s2
+  float s2_down;            // 2^-s2 (already folded into W1; kept for inspection)
   float pad[2];
 };
 static_assert(offsetof(PrepImage, escale) % 16 == 0, "escale is read as float4");

@@ -112,6 +112,23 @@ __device__ __forceinline__ void mbar_sleep(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// Shared-window (u32) address forms: callers hoist the CTA's shared base once
+// so barrier addresses are plain adds, not generic->shared conversions.
+__device__ __forceinline__ void mbar_wait_at(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LOPT_WAITA_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LOPT_WAITA_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_at(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
+
 // ---- MMA --------------------------------------------------------------------
 // D[tmem] (+)= A * B, A and B described by shared-memory descriptors.
 __device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
