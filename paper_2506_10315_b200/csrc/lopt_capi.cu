@@ -40,7 +40,7 @@ namespace {
 
 constexpr int64_t kStrictStatChunk = 8192;
 constexpr int64_t kStrictApplyChunk = 4096;
-constexpr int64_t kFactorTileElems = 65536;
+constexpr int64_t kFactorTileElems = 131072;   // 256 rows x 512 columns per CTA
 
 struct Region {
   size_t off = 0, bytes = 0;

@@ -58,9 +58,9 @@ __device__ __forceinline__ int64_t col_of(int64_t b0, int lane, int k) {
 // element-range mask of a sharded plan is applied only on rows that straddle
 // [lo, hi).  A non-finite gradient shows up as a non-finite row sum.
 template <bool VEC>
-__device__ void factor_tile(const DevicePlan &P, const FactorItem &it, const TensorDesc &T) {
+__device__ void factor_tile(const DevicePlan &P, const FactorItem &it, const TensorDesc &T,
+                            double (*colbuf)[kStripCols]) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ double colbuf[kStripCols];
   __shared__ uint32_t bad_s;
   if (tid == 0) bad_s = 0;
   double colacc[16];
@@ -97,21 +97,19 @@ __device__ void factor_tile(const DevicePlan &P, const FactorItem &it, const Ten
       }
     }
   }
-  // combine the warps' column partials in warp order
-  __syncthreads();
-  for (int w = 0; w < kFactorWarps; w++) {
-    if (warp == w) {
+  // combine the warps' column partials: every warp parks its 16 columns in
+  // its own row of shared memory, one barrier, then each thread sums the
+  // warps in warp order (fixed order: bit-reproducible)
 #pragma unroll
-      for (int k = 0; k < 16; k++) {
-        const int j = (int)(col_of<VEC>(0, lane, k));
-        colbuf[j] = (w == 0) ? colacc[k] : colbuf[j] + colacc[k];
-      }
-    }
-    __syncthreads();
-  }
+  for (int k = 0; k < 16; k++) colbuf[warp][(int)col_of<VEC>(0, lane, k)] = colacc[k];
+  __syncthreads();
   const int64_t width = it.b1 - it.b0;
-  for (int j = tid; j < width; j += kFactorThreads)
-    T.colpart[(int64_t)it.rowblock * n + it.b0 + j] = colbuf[j];
+  for (int j = tid; j < width; j += kFactorThreads) {
+    double c = colbuf[0][j];
+#pragma unroll
+    for (int w = 1; w < kFactorWarps; w++) c += colbuf[w][j];
+    T.colpart[(int64_t)it.rowblock * n + it.b0 + j] = c;
+  }
   if (bad) atomicOr(&bad_s, 1u);
   __syncthreads();
   if (tid == 0 && bad_s) flag_nonfinite(P, it.tensor);
@@ -156,15 +154,16 @@ __device__ void factor_vector(const DevicePlan &P, const FactorItem &it, const T
 
 // One CTA per item (the loop also allows a persistent launch).
 __global__ void __launch_bounds__(kFactorThreads, 2) factor_partials_kernel(DevicePlan P) {
+  __shared__ double colbuf[kFactorWarps][kStripCols];   // one copy for both tile variants
   for (int item = blockIdx.x; item < P.n_factor_items; item += gridDim.x) {
     const FactorItem it = P.factor_items[item];
     const TensorDesc T = P.tensors[it.tensor];
     if (T.n == 1) {
       factor_vector(P, it, T);
     } else if ((T.n & 3) == 0 && (reinterpret_cast<uintptr_t>(T.grad) & 15) == 0) {
-      factor_tile<true>(P, it, T);
+      factor_tile<true>(P, it, T, colbuf);
     } else {
-      factor_tile<false>(P, it, T);
+      factor_tile<false>(P, it, T, colbuf);
     }
     __syncthreads();   // shared scratch is reused by the next item
   }
