@@ -110,8 +110,15 @@ def dist_setup(args):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # LOPT_DIST_BACKEND=gloo with LOPT_SHARE_GPU=1 runs all ranks on cuda:0
+        # (a functional check of the multi-rank path on a one-GPU box)
+        backend = os.environ.get("LOPT_DIST_BACKEND", "nccl")
+        dev = 0 if os.environ.get("LOPT_SHARE_GPU") else local
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
@@ -130,7 +137,8 @@ def max_over_ranks(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -302,8 +310,10 @@ def reference_arm(args, world, rank):
     from oracle import oracle as O
 
     O.lib()
-    r = run_cpu_oracle(args.workload, args.feature_set, args.cpu_budget, args.steps,
-                       max(1, min(args.warmup, 1)))
+    # size each step's sample so the whole --steps run stays around two minutes
+    # (~1.5 Mparams/s on 16 host cores): at most --cpu-budget params per step
+    budget = int(max(1_000_000, min(args.cpu_budget, 12_000_000 * 15 // (args.steps + 1))))
+    r = run_cpu_oracle(args.workload, args.feature_set, budget, args.steps, 1)
     value = r["params"] / r["step_s"] / 1e9
     sample = (f"{r['tensors']} of the {args.workload} tensors, {r['params']} params "
               f"(largest-first prefix of the census), median of {r['steps']} steps")
@@ -358,11 +368,11 @@ def main():
     n_tensors, n_params = census(args.workload)
     peaks, peak_kind = measured_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK))
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", torch.cuda.current_device())
     params, grads = make_model(args.workload, dev, seed=0)
 
     opt = build_optimizer(params, args.feature_set, args.mode, world)
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         ms, phases, launches = time_device(opt, params, grads, args.steps, args.warmup, world)
     clocks = clk.summary()
     value = n_params * args.steps / (ms / 1e3) / 1e9
