@@ -211,13 +211,19 @@ def time_device(opt, params, grads, steps, warmup, world):
     barrier(world)
     ms = start.elapsed_time(end)
     opt.phase_events = []
-    for _ in range(steps):
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    marks[0].record()
+    for k in range(steps):
         opt.step(**kw)
+        marks[k + 1].record()
     torch.cuda.synchronize()
     phases = {}
     for name, a, b in opt.phase_events:
         phases.setdefault(name, []).append(a.elapsed_time(b))
     opt.phase_events = None
+    per_step = sorted(marks[k].elapsed_time(marks[k + 1]) for k in range(steps))
+    q = lambda f: per_step[min(len(per_step) - 1, int(f * (len(per_step) - 1) + 0.5))]  # noqa: E731
+    phases["_step_quantiles"] = [q(0.1), q(0.5), q(0.9)]
     launches = sum(pl.launches_last_step() for pl in opt.plans())
     return max_over_ranks(ms, world), phases, launches
 
@@ -379,9 +385,10 @@ def main():
     apply_ms = statistics.mean(phases.get("apply", [float("nan")]))
     local_params = sum(pl.local_elements() for pl in opt.plans())
     achieved = ALGO_BYTES_PER_PARAM * local_params / (apply_ms / 1e3) / 1e9
+    quant = phases.pop("_step_quantiles", None)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": None, "kernel": "apply (phase 2)",
-                "peak_source": peak_kind,
+                "peak_source": peak_kind, "frac_vs_8tbs_spec": achieved / 8000.0,
                 "phase_ms": {k: statistics.mean(v) for k, v in phases.items()},
                 "step_frac_of_roofline": (ALGO_BYTES_PER_PARAM * n_params / (ms / args.steps / 1e3)
                                           / 1e9) / hbm_peak}
@@ -425,6 +432,7 @@ def main():
                              "bank of 4 MLPs)",
                 "value": n_params * args.steps / (vms / 1e3) / 1e9, "unit": "Gparams/s",
                 "ms_per_step": vms / args.steps,
+                "step_ms_p10_p50_p90": vph.pop("_step_quantiles", None),
                 "phase_ms": {k: statistics.mean(v) for k, v in vph.items()}}
 
     cpu = None
@@ -441,6 +449,7 @@ def main():
             "metric": metric_name(args), "value": value, "unit": "Gparams/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "step_ms_p10_p50_p90": quant,
             "scaling": "strong" if world > 1 else "none", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": args.workload, "feature_set": args.feature_set,
