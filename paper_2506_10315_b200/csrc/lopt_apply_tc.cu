@@ -102,12 +102,12 @@ struct __align__(1024) ApplySmem {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tc::smem_u32(bar)) : "memory");
 }
-// One arrival per warp (the barriers count warps, not threads): the lanes'
-// prior writes are ordered before the elected lane's release by __syncwarp.
+// Hand-off arrival of a math warpgroup: every lane arrives (count 128), each
+// after its own tcgen05.wait / fence, so no intra-warp sync is needed.
 __device__ __forceinline__ void warp_arrive(uint64_t *bar) {
-  __syncwarp();
-  if (tc::elect_one()) mbar_arrive(bar);
-  __syncwarp();
+  // every thread arrives (barriers count 128 per warpgroup): one instruction
+  // per lane instead of a syncwarp / elect / arrive / syncwarp sequence
+  mbar_arrive(bar);
 }
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tc::smem_u32(bar)),
@@ -409,17 +409,17 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
   if (tid == 0) {
     for (int r = 0; r < kRing; r++) {
       tc::mbar_init(&S.full[r], 1);
-      tc::mbar_init(&S.data_free[r], 4);
+      tc::mbar_init(&S.data_free[r], 128);
     }
     for (int b = 0; b < kImgs; b++) tc::mbar_init(&S.img_full[b], 1);
     for (int w = 0; w < kWGsC; w++)
       for (int q = 0; q < 4; q++) S.c_done[w][q] = -1;
     for (int s = 0; s < kSlots; s++) {
-      tc::mbar_init(&S.op_ready[s], 4);
+      tc::mbar_init(&S.op_ready[s], 128);
       tc::mbar_init(&S.acc1_full[s], 1);
-      tc::mbar_init(&S.h_ready[s], 4);
+      tc::mbar_init(&S.h_ready[s], 128);
       tc::mbar_init(&S.acc2_full[s], 1);
-      tc::mbar_init(&S.slot_free[s], 4);
+      tc::mbar_init(&S.slot_free[s], 128);
     }
     tc::mbar_fence_init();
   }
