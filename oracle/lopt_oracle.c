@@ -368,8 +368,54 @@ static void mlp_lane(const lo_mlp *w, const float *w1s, const float *x, float *d
   *mag = mg;
 }
 
+/* engine.py:441-480 _mlp_lanes over LANES elements at once, as the
+ * reference blocks them (64 lanes): every lane's outputs are the same
+ * sequential fma chains as mlp_lane (bitwise), but the innermost loop runs
+ * across lanes, so the compiler vectorizes it (8 lanes per AVX2 FMA). */
+#define LANES 64
+static void mlp_lanes(const lo_mlp *w, const float *w1s, const float (*x)[LANES], int nl,
+                      float *dir, float *mag) {
+  float h1[LO_MAX_HIDDEN][LANES], h2[LO_MAX_HIDDEN][LANES];
+  for (int o = 0; o < w->h1; o++)
+    for (int l = 0; l < LANES; l++) h1[o][l] = w->b1[o];
+  for (int j = 0; j < w->d; j++)
+    for (int o = 0; o < w->h1; o++) {
+      const float c = w1s[o * w->d + j];
+      for (int l = 0; l < LANES; l++) h1[o][l] = fmaf(c, x[j][l], h1[o][l]);
+    }
+  for (int o = 0; o < w->h1; o++)
+    for (int l = 0; l < LANES; l++)
+      if (h1[o][l] < 0.0f) h1[o][l] = 0.0f;
+  for (int o = 0; o < w->h2; o++)
+    for (int l = 0; l < LANES; l++) h2[o][l] = w->b2[o];
+  for (int j = 0; j < w->h1; j++)
+    for (int o = 0; o < w->h2; o++) {
+      const float c = w->w2[o * w->h1 + j];
+      for (int l = 0; l < LANES; l++) h2[o][l] = fmaf(c, h1[j][l], h2[o][l]);
+    }
+  for (int o = 0; o < w->h2; o++)
+    for (int l = 0; l < LANES; l++)
+      if (h2[o][l] < 0.0f) h2[o][l] = 0.0f;
+  float d[LANES], mg[LANES];
+  for (int l = 0; l < LANES; l++) {
+    d[l] = w->b3[0];
+    mg[l] = w->b3[1];
+  }
+  for (int j = 0; j < w->h2; j++) {
+    const float cd = w->w3[j], cm = w->w3[w->h2 + j];
+    for (int l = 0; l < LANES; l++) {
+      d[l] = fmaf(cd, h2[j][l], d[l]);
+      mg[l] = fmaf(cm, h2[j][l], mg[l]);
+    }
+  }
+  for (int l = 0; l < nl; l++) {
+    dir[l] = d[l];
+    mag[l] = mg[l];
+  }
+}
+
 /* engine.py:657-710 fused_apply (pass 2) over [lo, hi): writes out, returns
- * max |update| through *maxabs. */
+ * max |update| through *maxabs.  Elements go through the MLP 64 at a time. */
 static int apply_view(const lo_view *s, const lo_mlp *w, const double *sumsq,
                       int64_t count, float lr, int64_t lo, int64_t hi, float *out,
                       float *maxabs_out) {
@@ -384,20 +430,32 @@ static int apply_view(const lo_view *s, const lo_mlp *w, const double *sumsq,
   const float alpha = w->alpha, beta_out = w->beta_out;
   const float ds = (float)w->update_sign * lr;
   float feat[LO_MAX_FEAT];
+  float x[LO_MAX_FEAT][LANES];
+  float dir[LANES], mag[LANES];
   float maxabs = 0.0f;
   const int64_t n = s->n;
-  for (int64_t i = lo; i < hi; i++) {
-    const int64_t a = i / n, b = i - a * n;
-    fill_features(s, a, b, feat);
-    float dir, mag;
-    mlp_lane(w, w1s, feat, &dir, &mag);
-    const float t = mag * alpha;
-    const float e = expf(t);
-    const float upd = (dir * e) * beta_out;
-    const float du = ds * upd;
-    out[i] = s->W[i] + du;
-    const float au = fabsf(du);
-    if (au > maxabs) maxabs = au;
+  for (int64_t i0 = lo; i0 < hi; i0 += LANES) {
+    const int nl = (int)(hi - i0 < LANES ? hi - i0 : LANES);
+    for (int l = 0; l < LANES; l++) {
+      if (l < nl) {
+        const int64_t i = i0 + l, a = i / n, b = i - a * n;
+        fill_features(s, a, b, feat);
+        for (int j = 0; j < d; j++) x[j][l] = feat[j];
+      } else {
+        for (int j = 0; j < d; j++) x[j][l] = 0.0f;
+      }
+    }
+    mlp_lanes(w, w1s, (const float (*)[LANES])x, nl, dir, mag);
+    for (int l = 0; l < nl; l++) {
+      const int64_t i = i0 + l;
+      const float t = mag[l] * alpha;
+      const float e = expf(t);
+      const float upd = (dir[l] * e) * beta_out;
+      const float du = ds * upd;
+      out[i] = s->W[i] + du;
+      const float au = fabsf(du);
+      if (au > maxabs) maxabs = au;
+    }
   }
   free(w1s);
   *maxabs_out = maxabs;
