@@ -441,6 +441,26 @@ def main():
                 "step_ms_p10_p50_p90": vph.pop("_step_quantiles", None),
                 "phase_ms": {k: statistics.mean(v) for k, v in vph.items()}}
 
+    # context: the same parameters stepped by torch's fused
+    # AdamW, the usual hand-designed optimizer, on the same device
+    adam = None
+    if world == 1 and not args.no_velo:
+        params, grads = make_model(args.workload, dev, seed=0)
+        for p, g in zip(params, grads):
+            p.grad = g
+        aopt = torch.optim.AdamW(params, lr=1e-3, fused=True)
+        for _ in range(args.warmup):
+            aopt.step()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(args.steps):
+            aopt.step()
+        a1.record()
+        torch.cuda.synchronize()
+        adam = {"torch_adamw_fused_ms_per_step": a0.elapsed_time(a1) / args.steps}
+        del aopt, params, grads
+
     cpu = None
     if not args.no_cpu and world == 1:
         r = run_cpu_oracle(args.workload, args.feature_set, args.cpu_budget or n_params, 3, 1)
@@ -465,6 +485,7 @@ def main():
                        "l2": f"inputs larger than L2 (each f32 array {n_params * 4 / 1e6:.0f} MB "
                              f"> 126 MB)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "velo": velo,
+            "context": adam,
             "clocks": clocks, "gpu_launches": launches * args.steps,
         }
         print(json.dumps(line), flush=True)
