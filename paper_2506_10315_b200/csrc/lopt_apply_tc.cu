@@ -234,8 +234,7 @@ struct Producer {
     }
   }
 
-  __device__ __forceinline__ void stage(Stage &st, uint64_t *full, int img, int img_par,
-                                        int dbg = 0) {
+  __device__ __forceinline__ void stage(Stage &st, uint64_t *full, int img, int img_par) {
     TileMeta mt;
     mt.j = j;
     mt.b0 = b0;
@@ -260,10 +259,6 @@ struct Producer {
     st.meta = mt;
     const uint32_t nv = (uint32_t)(v1 - v0);
     const uint32_t bytes = (fast ? 24u * nv : 0u) + (rb ? 64u : 0u);
-    if (dbg & 16) {
-      mbar_arrive(full);
-      return;
-    }
     mbar_arrive_tx(full, bytes);
     if (fast && nv > 0) {
       bulk_g2s(&st.th[v0], theta + el0 + v0, 4 * nv, full);
@@ -495,7 +490,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
         if (i % kProducers == p) {
           if (rc.wrapped) WAIT(&S.data_free[rc.i], rc.phase ^ 1u, 1);
           trace(P, i, 0);
-          pr.stage(S.stage[rc.i], &S.full[rc.i], img, (int)((par_bits >> img) & 1u), P.dbg);
+          pr.stage(S.stage[rc.i], &S.full[rc.i], img, (int)((par_bits >> img) & 1u));
         }
         pr.advance(P);
         rc.next();
@@ -613,10 +608,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       if (sc.wrapped) WAIT(&S.slot_free[sc.i], sc.phase ^ 1u, 6);
       tc::fence_after_sync();
       const uint32_t ta = tbase + lane_addr + 64 * sc.i;
-      if (!(P.dbg & 2)) {
-        tc::tmem_st16(ta, ev);
-        tc::tmem_st16(ta + 16, bv);
-      }
+      tc::tmem_st16(ta, ev);
+      tc::tmem_st16(ta + 16, bv);
       tc::tmem_st_wait();
       tc::fence_before_sync();
       if (warp == 0) trace(P, i, 2);
@@ -639,21 +632,14 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
 #pragma unroll
       for (int half = 0; half < 2; half++) {
         uint32_t h[16];
-        if (P.dbg & 2) {
-#pragma unroll
-          for (int q = 0; q < 16; q++) h[q] = __float_as_uint((float)(q + i));
-        } else {
-          tc::tmem_ld16(ta + 32 + 16 * half, h);
-          tc::tmem_ld_wait();
-        }
+        tc::tmem_ld16(ta + 32 + 16 * half, h);
+        tc::tmem_ld_wait();
         uint32_t hi[8], lo[8];
 #pragma unroll
         for (int q = 0; q < 8; q++)
           relu_split2(__uint_as_float(h[2 * q]), __uint_as_float(h[2 * q + 1]), hi[q], lo[q]);
-        if (!(P.dbg & 2)) {
-          tc::tmem_st8(ta + 8 * half, hi);
-          tc::tmem_st8(ta + 16 + 8 * half, lo);
-        }
+        tc::tmem_st8(ta + 8 * half, hi);
+        tc::tmem_st8(ta + 16 + 8 * half, lo);
       }
       tc::tmem_st_wait();
       tc::fence_before_sync();
@@ -695,12 +681,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       tc::fence_after_sync();
       if (warp == kWarpC) trace(P, i, 6);
       uint32_t h2[32];
-      if (P.dbg & 2) {
-#pragma unroll
-        for (int q = 0; q < 32; q++) h2[q] = __float_as_uint(w * (float)q);
-      } else {
-        tc::tmem_ld32(tbase + lane_addr + 64 * sc.i + 32, h2);
-      }
+      tc::tmem_ld32(tbase + lane_addr + 64 * sc.i + 32, h2);
       tc::tmem_ld_wait();
       tc::fence_before_sync();
       warp_arrive(&S.slot_free[sc.i]);
