@@ -165,19 +165,31 @@ def build_optimizer(params, feature_set, mode, world):
     """feature_set "velo" is the full VeLO optimizer (VELO_MLP features + the
     per-tensor LSTM hypernetwork mixing a bank of MLPs); "small_fc_lopt" and
     "velo_mlp" are the single-MLP learned optimizers."""
+    # N > 1: the parameter exchange is fused into the apply kernel (stores to
+    # the peers' IPC-mapped arenas over NVLink) unless LOPT_GATHER=nccl
+    gather = os.environ.get("LOPT_GATHER", "p2p" if mode == "fast" else "nccl")
     if feature_set == "velo":
         if world > 1:
             from paper_2506_10315_b200.dist import ShardedVeLO
 
-            return ShardedVeLO(params, mode=mode, check_errors=False)
+            try:
+                return ShardedVeLO(params, mode=mode, check_errors=False, gather=gather)
+            except Exception as e:  # noqa: BLE001
+                print(f"bench: p2p gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
+                return ShardedVeLO(params, mode=mode, check_errors=False)
         from paper_2506_10315_b200.velo import VeLO_CUDA
 
         return VeLO_CUDA(params, mode=mode, check_errors=False)
     if world > 1:
         from paper_2506_10315_b200.dist import ShardedLearnedOptimizer
 
-        return ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
-                                       check_errors=False)
+        try:
+            return ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
+                                           check_errors=False, gather=gather)
+        except Exception as e:  # noqa: BLE001
+            print(f"bench: p2p gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
+            return ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
+                                           check_errors=False)
     from paper_2506_10315_b200 import LearnedOptimizer
 
     return LearnedOptimizer(params, feature_set=feature_set, mode=mode, check_errors=False)
@@ -384,6 +396,7 @@ def main():
     params, grads = make_model(args.workload, dev, seed=0)
 
     opt = build_optimizer(params, args.feature_set, args.mode, world)
+    gather_used = getattr(opt, "gather", "nccl")
     clk = ClockSampler(torch.cuda.current_device())
     clk.__enter__()   # sampled through the timed steps, the phase pass and the e2e run
     ms, phases, launches = time_device(opt, params, grads, args.steps, args.warmup, world)
@@ -481,7 +494,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": args.workload, "feature_set": args.feature_set,
                        "mode": args.mode, "tensors": n_tensors, "params": n_params,
-                       "parallelism": f"element-sharded x{world}" if world > 1 else "single",
+                       "parallelism": (f"element-sharded x{world}, param exchange "
+                                       f"{gather_used}") if world > 1 else "single",
                        "l2": f"inputs larger than L2 (each f32 array {n_params * 4 / 1e6:.0f} MB "
                              f"> 126 MB)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "velo": velo,

@@ -162,6 +162,17 @@ int lopt_selftest_expf(const float *x, float *y, int64_t n, void *stream);
  * `rounds` commit/wait round trips; out[0] = SM cycles per round. */
 int lopt_probe_umma(int32_t batch, int32_t rounds, long long *out, void *stream);
 
+/* Fused parameter all-gather over NVLink (sharded step, replaces the
+ * all-gather of distsim.py:523-530): every parameter the fast-mode apply pass
+ * writes is also stored to `count` (<= LOPT_MAX_PEERS) peer copies at
+ * byte offset deltas[p] from its local address -- the peers' parameter arenas
+ * mapped into this process (CUDA IPC / symmetric memory), so the parameter
+ * exchange rides on the apply kernel's own stores instead of a separate
+ * collective.  count = 0 disables it.  The caller orders the peers' writes
+ * before the next use of the parameters (a cross-rank barrier after the step). */
+#define LOPT_MAX_PEERS 7
+int lopt_set_peers(lopt_plan *plan, int32_t count, const int64_t *deltas);
+
 const char *lopt_version(void);
 int lopt_num_kernels_launched_last_step(const lopt_plan *plan);
 

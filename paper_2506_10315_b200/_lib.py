@@ -33,7 +33,7 @@ EXPORTS = [
     "lopt_step", "lopt_factor_sums_ptr", "lopt_stat_sums_ptr", "lopt_status_ptr",
     "lopt_read_status", "lopt_debug_ptrs", "lopt_version",
     "lopt_num_kernels_launched_last_step", "lopt_velo_mix", "lopt_selftest_umma",
-    "lopt_probe_umma", "lopt_selftest_expf",
+    "lopt_probe_umma", "lopt_selftest_expf", "lopt_set_peers",
 ]
 
 
@@ -124,6 +124,7 @@ def lib(required: bool = True):
     L.lopt_velo_mix.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, vp]
     L.lopt_selftest_umma.argtypes = [i32, i32, vp, vp, vp, vp]
     L.lopt_probe_umma.argtypes = [i32, i32, vp, vp]
+    L.lopt_set_peers.argtypes = [vp, i32, vp]
     L.lopt_selftest_expf.argtypes = [vp, vp, ctypes.c_int64, vp]
     for name in EXPORTS:
         f = getattr(L, name)

@@ -653,6 +653,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     const float alpha_log2e = P.alpha * 1.4426950408889634f;
     const float dsb = P.step->ds * P.beta_out;
     const float decay = P.step->apply_decay != 0 ? P.step->decay : 1.0f;
+    const int n_peers = P.n_peers;
     int red_j = -1;
     float red_max = 0.0f, red_out = 0.0f;   // max |delta|, NaN-propagating max |theta'|
     Stride<kRing, kStep> rc(r0);
@@ -715,6 +716,10 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
         red_max = fmaxf(red_max, fabsf(du));
         red_out = max_nan_abs(red_out, out);
         *tp = out;
+        // fused all-gather: the same value into every peer's copy (NVLink
+        // stores through the peers' mapped arenas)
+        for (int q = 0; q < n_peers; q++)
+          *reinterpret_cast<float *>(reinterpret_cast<char *>(tp) + P.peer_delta[q]) = out;
       }
       rc.next();
       sc.next();
@@ -724,6 +729,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
         atomicMax(reinterpret_cast<unsigned int *>(&P.maxabs[red_j]), __float_as_uint(red_max));
       if (!(red_out <= 3.402823466e38f)) atomicOr(&P.status[red_j], LOPT_STATUS_NONFINITE_PARAM);
     }
+    if (n_peers > 0) __threadfence_system();   // peer stores performed before the caller's barrier
   }
   tc::fence_before_sync();
   __syncthreads();

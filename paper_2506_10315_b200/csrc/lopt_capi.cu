@@ -538,6 +538,14 @@ int lopt_velo_mix(lopt_plan *p, const float *hyper, float *lstm_state, const flo
   return st;
 }
 
+int lopt_set_peers(lopt_plan *p, int32_t count, const int64_t *deltas) {
+  if (!p || count < 0 || count > LOPT_MAX_PEERS || (count > 0 && !deltas)) return LOPT_ERR_INVALID;
+  if (count > 0 && p->cfg.mode != LOPT_MODE_FAST) return LOPT_ERR_UNSUPPORTED;
+  p->dp.n_peers = count;
+  for (int k = 0; k < LOPT_MAX_PEERS; k++) p->dp.peer_delta[k] = k < count ? deltas[k] : 0;
+  return LOPT_OK;
+}
+
 int lopt_num_kernels_launched_last_step(const lopt_plan *p) {
   return p ? p->launches_last_step : 0;
 }

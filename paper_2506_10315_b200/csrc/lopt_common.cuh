@@ -110,7 +110,8 @@ struct DevicePlan {
   int64_t n_tiles;        // 128-element tiles over all tensors
   unsigned char *prep;    // per-tensor PrepImage (B operands, layer-3 weights)
   double *bcsum;          // [count x d_feat] closed-form sums of broadcast features
-  int32_t dbg, pad_dbg;   // timing experiments only (LOPT_APPLY_DEBUG), 0 in production
+  int32_t dbg, n_peers;   // dbg: timing experiments only (LOPT_APPLY_DEBUG), 0 in production
+  int64_t peer_delta[LOPT_MAX_PEERS];   // fused all-gather: byte offsets of the peer copies
 };
 
 __host__ __device__ inline int weight_stride(int d, int h1, int h2) {

@@ -79,18 +79,37 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
     ranks at construction; gradients are expected to be already reduced
     (e.g. DDP), of which each rank reads only its own slice."""
 
-    def __init__(self, params, *args, process_group=None, **kw):
+    def __init__(self, params, *args, process_group=None, gather: str = "nccl", **kw):
         super().__init__(params, *args, **kw)
         self.pg = process_group
         self.world = dist.get_world_size(self.pg)
         self.rank = dist.get_rank(self.pg)
         if len(self.param_groups) != 1:
             raise ValueError("the sharded step supports one parameter group")
+        if gather not in ("nccl", "p2p"):
+            raise ValueError(f"unknown gather {gather!r}")
+        self.gather = gather
         ps = self.param_groups[0]["params"]
         sizes = [p.numel() for p in ps]
         ranges, S, padded = flat_shard_ranges(sizes, self.world, self.rank)
         dev = ps[0].device
-        self.flat = torch.zeros(padded, dtype=torch.float32, device=dev)
+        self._peers = None
+        if gather == "p2p":
+            # every rank maps every other rank's parameter arena (CUDA IPC;
+            # NVLink peer access between GPUs) and the apply kernel stores each
+            # updated parameter into all of them, so no all-gather is launched
+            from torch.multiprocessing.reductions import reduce_tensor
+
+            if self.mode != "fast":
+                raise ValueError("gather='p2p' needs mode='fast'")
+            self.flat = torch.zeros(padded, dtype=torch.float32, device=dev)
+            handles = [None] * self.world
+            dist.all_gather_object(handles, reduce_tensor(self.flat), group=self.pg)
+            self._peers = [fn(*args) for r, (fn, args) in enumerate(handles) if r != self.rank]
+            base = self.flat.data_ptr()
+            self.set_peer_copies([q.data_ptr() - base for q in self._peers])
+        else:
+            self.flat = torch.zeros(padded, dtype=torch.float32, device=dev)
         off = 0
         for p, n in zip(ps, sizes):
             self.flat[off:off + n].copy_(p.data.view(-1))
@@ -161,7 +180,12 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         if self._after_stats is not None:
             timed("hypernet", lambda: self._after_stats(gi, plan, params))
         timed("apply", plan.apply)
-        timed("param_gather", self._gather)
+        if self._peers is not None:
+            # the peers' stores into this arena happened inside their apply
+            # kernels; one cross-rank barrier orders them before any read
+            timed("param_gather", self._peer_barrier)
+        else:
+            timed("param_gather", self._gather)
 
     def _nccl(self) -> bool:
         return dist.get_backend(self.pg) == "nccl"
@@ -173,6 +197,18 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
             h = t.cpu()
             dist.all_reduce(h, group=self.pg)
             t.copy_(h)
+
+    def _peer_barrier(self):
+        if self._nccl():
+            # stream-ordered: completes after every rank's apply kernel (whose
+            # peer stores end with a system-scope fence)
+            t = getattr(self, "_barrier_buf", None)
+            if t is None:
+                t = self._barrier_buf = torch.zeros(1, device=self.flat.device)
+            dist.all_reduce(t, group=self.pg)
+        else:
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.pg)
 
     def _gather(self):
         S = self.slice_len

@@ -187,6 +187,13 @@ class StepPlan:
         self.set_step(lr, weight_decay, t)
         _lib.check(self.L.lopt_step(self.h, None, _stream_handle()), "step")
 
+    def set_peers(self, deltas):
+        """Fused parameter all-gather: the apply pass also stores every updated
+        parameter at these byte offsets from its local address (the peers'
+        mapped parameter arenas).  An empty list disables it."""
+        arr = (ctypes.c_int64 * max(1, len(deltas)))(*[int(d) for d in deltas])
+        _lib.check(self.L.lopt_set_peers(self.h, len(deltas), arr), "set_peers")
+
     def local_elements(self) -> int:
         return sum(s.hi - s.lo for s in self.slots)
 

@@ -134,6 +134,8 @@ class LearnedOptimizer(torch.optim.Optimizer):
         cached = self._plans.get(gi)
         if cached is None or cached[0] != key:
             plan = StepPlan(slots, self.spec, weights, mode=self.mode)
+            if getattr(self, "_peer_deltas", None):
+                plan.set_peers(self._peer_deltas)
             self._plans[gi] = (key, plan, [s.grad.data_ptr() for s in slots])
         else:
             _, plan, ptrs = cached
@@ -205,6 +207,17 @@ class LearnedOptimizer(torch.optim.Optimizer):
     def plans(self):
         """The StepPlans of the parameter groups (one per group)."""
         return [entry[1] for entry in self._plans.values()]
+
+    def set_peer_copies(self, deltas):
+        """Fused parameter replication (fast mode): the apply pass also stores
+        every updated parameter at these byte offsets from its local address
+        -- peer GPUs' parameter arenas mapped into this process.  Used by the
+        sharded optimizer's NVLink gather; [] disables it."""
+        if deltas and self.mode != "fast":
+            raise OptimError("peer copies need mode='fast'")
+        self._peer_deltas = [int(d) for d in deltas]
+        for _, plan, _ in self._plans.values():
+            plan.set_peers(self._peer_deltas)
 
     # -- host-buffer step (offload) ------------------------------------------
     @torch.no_grad()

@@ -32,7 +32,7 @@ def _init(seed=0):
     return init, grads
 
 
-def _worker(rank, world, port, mode, fs, q):
+def _worker(rank, world, port, mode, fs, q, gather="nccl"):
     import sys
     import traceback
 
@@ -50,7 +50,8 @@ def _worker(rank, world, port, mode, fs, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         init, grads = _init()
         params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
-        opt = ShardedLearnedOptimizer(params, feature_set=fs, mode=mode, weight_decay=0.01)
+        opt = ShardedLearnedOptimizer(params, feature_set=fs, mode=mode, weight_decay=0.01,
+                                      gather=gather)
         for gs in grads:
             for p, g in zip(params, gs):
                 p.grad = torch.from_numpy(g).cuda()
@@ -63,9 +64,15 @@ def _worker(rank, world, port, mode, fs, q):
         q.put((rank, traceback.format_exc(), 0))
 
 
-@pytest.mark.parametrize("mode,fs", [("strict", "small_fc_lopt"), ("fast", "velo_mlp"),
-                                     ("fast", "small_fc_lopt")])
-def test_sharded_equals_single_gpu(mode, fs):
+@pytest.mark.parametrize("mode,fs,gather", [("strict", "small_fc_lopt", "nccl"),
+                                            ("fast", "velo_mlp", "nccl"),
+                                            ("fast", "small_fc_lopt", "nccl"),
+                                            ("fast", "small_fc_lopt", "p2p")])
+def test_sharded_equals_single_gpu(mode, fs, gather):
+    """gather="p2p": the parameter arena in symmetric memory, the apply kernel
+    storing every updated parameter into the other rank's mapped arena (the
+    NVLink path; here both ranks map one device), one barrier instead of the
+    all-gather."""
     import torch
     import torch.multiprocessing as mp
 
@@ -84,7 +91,7 @@ def test_sharded_equals_single_gpu(mode, fs):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, fs, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, fs, q, gather)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]

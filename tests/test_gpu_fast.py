@@ -199,3 +199,45 @@ def test_step_host_matches_device_step(P, mode):
         assert h.numpy().tobytes() == q.detach().cpu().numpy().tobytes()
     for p, q in zip(a, b):
         assert oa.state[p]["quad"].cpu().numpy().tobytes() == ob.state[q]["quad"].cpu().numpy().tobytes()
+
+
+def test_fused_peer_copies_single_gpu(P):
+    """The fused all-gather path with stand-in peers: two more arenas on the
+    same device play the other ranks' parameter copies; after a fast step they
+    must hold exactly the updated parameters (same kernel stores, other
+    addresses), and the local result must equal a step without peers."""
+    import torch
+
+    shapes = [(128, 784), (128,), (10, 128), (10,), (33, 70)]
+    total = sum(int(np.prod(s)) for s in shapes)
+    rng = np.random.default_rng(4)
+    init = [np.asarray(rng.standard_normal(s) * 0.02, dtype=F32) for s in shapes]
+    grads = [np.asarray(rng.standard_normal(s) * 1e-3, dtype=F32) for s in shapes]
+
+    def build(arena):
+        ps, off = [], 0
+        for x, s in zip(init, shapes):
+            n = x.size
+            arena[off:off + n].copy_(torch.from_numpy(x.reshape(-1)))
+            ps.append(torch.nn.Parameter(arena[off:off + n].view(s)))
+            off += n
+        return ps
+
+    arena = torch.zeros(total, device="cuda")
+    peers = [torch.full((total,), 7.0, device="cuda") for _ in range(2)]
+    ps = build(arena)
+    opt = P.LearnedOptimizer(ps, mode="fast", weight_decay=0.01)
+    opt.set_peer_copies([q.data_ptr() - arena.data_ptr() for q in peers])
+    for p, g in zip(ps, grads):
+        p.grad = torch.from_numpy(g).cuda()
+    opt.step()
+    ref_arena = torch.zeros(total, device="cuda")
+    rs = build(ref_arena)
+    ropt = P.LearnedOptimizer(rs, mode="fast", weight_decay=0.01)
+    for p, g in zip(rs, grads):
+        p.grad = torch.from_numpy(g).cuda()
+    ropt.step()
+    torch.cuda.synchronize()
+    assert torch.equal(arena, ref_arena)
+    for q in peers:
+        assert torch.equal(q, arena)
