@@ -8,10 +8,14 @@
 // identical f64 sums it reproduces fused_apply bit for bit.  The fast mode
 // (lopt_fast.cu) is the product path; this one is the yardstick.
 #include "lopt_common.cuh"
+#include "lopt_tc.cuh"
 
 namespace lopt {
 
 constexpr int kStrictThreads = 256;
+// apply: two elements a thread (~214 registers, one CTA of 8 warps per SM;
+// 192 threads x 2 CTAs at 168 registers spilled and ran 27% slower)
+constexpr int kStrictApplyThreads = 256;
 
 // Flat element index -> (row, col) for a chunk that starts at e0.
 struct RowCol {
@@ -21,11 +25,35 @@ __device__ __forceinline__ RowCol split_index(int64_t e, int64_t n) {
   return {e / n, e % n};
 }
 
-__device__ __forceinline__ void load_elem(const TensorDesc &T, int64_t e, bool advanced,
-                                          const float *beta, Elem &x, float4 &newstate) {
-  x.w = T.theta[e];
-  x.g = T.grad[e];
-  const float4 s = T.state[e - T.lo];
+// One element's global inputs, loaded before any of them is used so that a
+// thread keeps two elements' loads in flight (the strict kernels run at one
+// or two warps per scheduler and are otherwise load-latency bound).
+struct RawElem {
+  float w, g;
+  float4 s, r0, r1, c0, c1;
+};
+
+__device__ __forceinline__ RawElem load_raw(const TensorDesc &T, int64_t e) {
+  RawElem r;
+  r.w = T.theta[e];
+  r.g = T.grad[e];
+  r.s = T.state[e - T.lo];
+  const RowCol rc = split_index(e, T.n);
+  const float4 *rt = reinterpret_cast<const float4 *>(T.rowtab + rc.a * kRowTab);
+  const float4 *ct = reinterpret_cast<const float4 *>(T.coltab + rc.b * kRowTab);
+  r.r0 = rt[0];
+  r.r1 = rt[1];
+  r.c0 = ct[0];
+  r.c1 = ct[1];
+  return r;
+}
+
+__device__ __forceinline__ void unpack_elem(const RawElem &r, bool advanced, const float *beta,
+                                            Elem &x, float4 &newstate, float *rowt,
+                                            float *colt) {
+  x.w = r.w;
+  x.g = r.g;
+  const float4 s = r.s;
   if (advanced) {
     x.m1 = s.x; x.m2 = s.y; x.m3 = s.z; x.v = s.w;
   } else {
@@ -36,12 +64,10 @@ __device__ __forceinline__ void load_elem(const TensorDesc &T, int64_t e, bool a
     x.v = ema(beta[3], __fsub_rn(1.0f, beta[3]), s.w, __fmul_rn(x.g, x.g));
   }
   newstate = make_float4(x.m1, x.m2, x.m3, x.v);
-}
-
-__device__ __forceinline__ void load_tab(const float *tab, int64_t i, float *out) {
-  const float4 lo = reinterpret_cast<const float4 *>(tab + i * kRowTab)[0];
-  const float4 hi = reinterpret_cast<const float4 *>(tab + i * kRowTab)[1];
-  out[0] = lo.x; out[1] = lo.y; out[2] = lo.z; out[3] = lo.w; out[4] = hi.x; out[5] = hi.y;
+  rowt[0] = r.r0.x; rowt[1] = r.r0.y; rowt[2] = r.r0.z; rowt[3] = r.r0.w;
+  rowt[4] = r.r1.x; rowt[5] = r.r1.y;
+  colt[0] = r.c0.x; colt[1] = r.c0.y; colt[2] = r.c0.z; colt[3] = r.c0.w;
+  colt[4] = r.c1.x; colt[5] = r.c1.y;
 }
 
 // Phase 1 (engine.py:619-654 fused_stats): per-element features, f64 sums of
@@ -60,20 +86,25 @@ stats_strict_kernel(DevicePlan P) {
   double acc[D];
 #pragma unroll
   for (int k = 0; k < D; k++) acc[k] = 0.0;
-  for (int64_t e = it.e0 + threadIdx.x; e < it.e1; e += kStrictThreads) {
+  auto accumulate = [&](const RawElem &r) {
     Elem x;
     float4 ns;
-    load_elem(T, e, P.state_advanced, P.beta, x, ns);
-    const RowCol rc = split_index(e, T.n);
     float rowt[6], colt[6], f[D];
-    load_tab(T.rowtab, rc.a, rowt);
-    load_tab(T.coltab, rc.b, colt);
+    unpack_elem(r, P.state_advanced, P.beta, x, ns, rowt, colt);
     strict_features<KIND>(x, rowt, colt, ts.mr, tf, f);
 #pragma unroll
     for (int k = 0; k < D; k++) {
       const double fv = (double)f[k];
       acc[k] = __fma_rn(fv, fv, acc[k]);
     }
+  };
+  for (int64_t e = it.e0 + threadIdx.x; e < it.e1; e += 2 * kStrictThreads) {
+    const int64_t eb = e + kStrictThreads;
+    const bool has_b = eb < it.e1;
+    const RawElem ra = load_raw(T, e);
+    const RawElem rb = load_raw(T, has_b ? eb : e);
+    accumulate(ra);
+    if (has_b) accumulate(rb);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -146,52 +177,59 @@ __device__ void load_strict_mlp(const DevicePlan &P, const TensorDesc &T, Strict
   __syncthreads();
 }
 
-// engine.py:441-480 _mlp_lanes for one element: fmaf chains in input order.
+// engine.py:441-480 _mlp_lanes, two elements a thread: lane .x is element A,
+// lane .y element B.  fma.rn.f32x2 is two independent correctly rounded fmas
+// and each weight is a broadcast operand (SASS FFMA2 R.F32), so every output
+// is the reference's fmaf chain in input order, bit for bit, while one
+// shared-memory weight load feeds four fmas and the FP32 pipe retires two
+// per issue slot.
 template <int D>
-__device__ __forceinline__ void strict_mlp(const StrictMlpSmem &S, const float *x, float &dir,
-                                           float &mag) {
-  float h1[kMaxHidden];
+__device__ __forceinline__ void strict_mlp2(const StrictMlpSmem &S, const float *fa,
+                                            const float *fb, float2 &dir, float2 &mag) {
+  float2 h1[kMaxHidden];
 #pragma unroll
-  for (int o = 0; o < kMaxHidden; o++) h1[o] = S.b1[o];
+  for (int o = 0; o < kMaxHidden; o++) h1[o] = make_float2(S.b1[o], S.b1[o]);
 #pragma unroll
   for (int j = 0; j < D; j++) {
-    const float xj = x[j];
+    const float2 xj = make_float2(fa[j], fb[j]);
     const float4 *wr = reinterpret_cast<const float4 *>(S.w1sT[j]);
 #pragma unroll
     for (int q = 0; q < kMaxHidden / 4; q++) {
       const float4 w = wr[q];
-      h1[4 * q + 0] = __fmaf_rn(w.x, xj, h1[4 * q + 0]);
-      h1[4 * q + 1] = __fmaf_rn(w.y, xj, h1[4 * q + 1]);
-      h1[4 * q + 2] = __fmaf_rn(w.z, xj, h1[4 * q + 2]);
-      h1[4 * q + 3] = __fmaf_rn(w.w, xj, h1[4 * q + 3]);
+      h1[4 * q + 0] = tc::fma2(make_float2(w.x, w.x), xj, h1[4 * q + 0]);
+      h1[4 * q + 1] = tc::fma2(make_float2(w.y, w.y), xj, h1[4 * q + 1]);
+      h1[4 * q + 2] = tc::fma2(make_float2(w.z, w.z), xj, h1[4 * q + 2]);
+      h1[4 * q + 3] = tc::fma2(make_float2(w.w, w.w), xj, h1[4 * q + 3]);
     }
   }
 #pragma unroll
-  for (int o = 0; o < kMaxHidden; o++)
-    if (h1[o] < 0.0f) h1[o] = 0.0f;
-  float h2[kMaxHidden];
+  for (int o = 0; o < kMaxHidden; o++) {
+    if (h1[o].x < 0.0f) h1[o].x = 0.0f;
+    if (h1[o].y < 0.0f) h1[o].y = 0.0f;
+  }
+  float2 h2[kMaxHidden];
 #pragma unroll
-  for (int o = 0; o < kMaxHidden; o++) h2[o] = S.b2[o];
+  for (int o = 0; o < kMaxHidden; o++) h2[o] = make_float2(S.b2[o], S.b2[o]);
 #pragma unroll
   for (int j = 0; j < kMaxHidden; j++) {
-    const float hj = h1[j];
     const float4 *wr = reinterpret_cast<const float4 *>(S.w2T[j]);
 #pragma unroll
     for (int q = 0; q < kMaxHidden / 4; q++) {
       const float4 w = wr[q];
-      h2[4 * q + 0] = __fmaf_rn(w.x, hj, h2[4 * q + 0]);
-      h2[4 * q + 1] = __fmaf_rn(w.y, hj, h2[4 * q + 1]);
-      h2[4 * q + 2] = __fmaf_rn(w.z, hj, h2[4 * q + 2]);
-      h2[4 * q + 3] = __fmaf_rn(w.w, hj, h2[4 * q + 3]);
+      h2[4 * q + 0] = tc::fma2(make_float2(w.x, w.x), h1[j], h2[4 * q + 0]);
+      h2[4 * q + 1] = tc::fma2(make_float2(w.y, w.y), h1[j], h2[4 * q + 1]);
+      h2[4 * q + 2] = tc::fma2(make_float2(w.z, w.z), h1[j], h2[4 * q + 2]);
+      h2[4 * q + 3] = tc::fma2(make_float2(w.w, w.w), h1[j], h2[4 * q + 3]);
     }
   }
-  float d = S.b3[0], m = S.b3[1];
+  float2 d = make_float2(S.b3[0], S.b3[0]), m = make_float2(S.b3[1], S.b3[1]);
 #pragma unroll
   for (int j = 0; j < kMaxHidden; j++) {
-    float hj = h2[j];
-    if (hj < 0.0f) hj = 0.0f;
-    d = __fmaf_rn(S.w3[0][j], hj, d);
-    m = __fmaf_rn(S.w3[1][j], hj, m);
+    float2 hj = h2[j];
+    if (hj.x < 0.0f) hj.x = 0.0f;
+    if (hj.y < 0.0f) hj.y = 0.0f;
+    d = tc::fma2(make_float2(S.w3[0][j], S.w3[0][j]), hj, d);
+    m = tc::fma2(make_float2(S.w3[1][j], S.w3[1][j]), hj, m);
   }
   dir = d;
   mag = m;
@@ -200,7 +238,7 @@ __device__ __forceinline__ void strict_mlp(const StrictMlpSmem &S, const float *
 // Phase 2 (engine.py:657-710 fused_apply + optim.py:171-172 decay): features,
 // MLP, update, decay; writes theta and the advanced accumulators.
 template <int KIND>
-__global__ void __launch_bounds__(kStrictThreads)
+__global__ void __launch_bounds__(kStrictApplyThreads)
 apply_strict_kernel(DevicePlan P) {
   constexpr int D = d_feat(KIND);
   const ChunkItem it = P.apply_items[blockIdx.x];
@@ -208,7 +246,7 @@ apply_strict_kernel(DevicePlan P) {
   const TensorScalars ts = P.tscal[it.tensor];
   __shared__ __align__(16) StrictMlpSmem S;
   __shared__ float tf[kTimeFeatures];
-  __shared__ float red[kStrictThreads / 32];
+  __shared__ float red[kStrictApplyThreads / 32];
   __shared__ uint32_t bad_s;
   if (threadIdx.x < kTimeFeatures) tf[threadIdx.x] = P.step->tf[threadIdx.x];
   if (threadIdx.x == 0) bad_s = 0;
@@ -221,18 +259,15 @@ apply_strict_kernel(DevicePlan P) {
   const bool apply_decay = P.step->apply_decay != 0;
   float maxabs = 0.0f;
   uint32_t bad = 0;
-  for (int64_t e = it.e0 + threadIdx.x; e < it.e1; e += kStrictThreads) {
-    Elem x;
-    float4 ns;
-    load_elem(T, e, P.state_advanced, P.beta, x, ns);
-    const RowCol rc = split_index(e, T.n);
-    float rowt[6], colt[6], f[D];
-    load_tab(T.rowtab, rc.a, rowt);
-    load_tab(T.coltab, rc.b, colt);
+  // element A = e, element B = e + kStrictApplyThreads (a duplicate of A, not
+  // stored, when it falls past the item's end)
+  auto features = [&](const RawElem &r, Elem &x, float4 &ns, float *f) {
+    float rowt[6], colt[6];
+    unpack_elem(r, P.state_advanced, P.beta, x, ns, rowt, colt);
     strict_features<KIND>(x, rowt, colt, ts.mr, tf, f);
-    float dir, mag;
-    strict_mlp<D>(S, f, dir, mag);
-    // engine.py:537-539: upd = dir * exp(mag*alpha) * beta; out = W + ds*upd
+  };
+  // engine.py:537-539: upd = dir * exp(mag*alpha) * beta; out = W + ds*upd
+  auto finish = [&](int64_t e, const Elem &x, const float4 &ns, float dir, float mag) {
     const float ex = glibc_expf(__fmul_rn(mag, alpha), S.exptab);
     const float upd = __fmul_rn(__fmul_rn(dir, ex), beta_out);
     const float du = __fmul_rn(ds, upd);
@@ -242,6 +277,21 @@ apply_strict_kernel(DevicePlan P) {
     if (apply_decay) out = __fmul_rn(out, decay);
     T.theta[e] = out;
     if (!P.state_advanced) T.state[e - T.lo] = ns;
+  };
+  for (int64_t e = it.e0 + threadIdx.x; e < it.e1; e += 2 * kStrictApplyThreads) {
+    const int64_t eb = e + kStrictApplyThreads;
+    const bool has_b = eb < it.e1;
+    Elem xa, xb;
+    float4 nsa, nsb;
+    float fa[D], fb[D];
+    const RawElem ra = load_raw(T, e);
+    const RawElem rb = load_raw(T, has_b ? eb : e);
+    features(ra, xa, nsa, fa);
+    features(rb, xb, nsb, fb);
+    float2 dir, mag;
+    strict_mlp2<D>(S, fa, fb, dir, mag);
+    finish(e, xa, nsa, dir.x, mag.x);
+    if (has_b) finish(eb, xb, nsb, dir.y, mag.y);
   }
   maxabs = fmaxf(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, 16));
   maxabs = fmaxf(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, 8));
@@ -253,7 +303,7 @@ apply_strict_kernel(DevicePlan P) {
   __syncthreads();
   if (threadIdx.x == 0) {
     float mx = 0.0f;
-    for (int w = 0; w < kStrictThreads / 32; w++) mx = fmaxf(mx, red[w]);
+    for (int w = 0; w < kStrictApplyThreads / 32; w++) mx = fmaxf(mx, red[w]);
     P.item_maxabs[blockIdx.x] = mx;
     if (bad_s) atomicOr(&P.status[it.tensor], LOPT_STATUS_NONFINITE_PARAM);
   }
@@ -293,9 +343,9 @@ void launch_stats_reduce(const DevicePlan &P, cudaStream_t s) {
 void launch_strict_apply(const DevicePlan &P, cudaStream_t s) {
   if (P.n_apply_items == 0) return;
   if (P.kind == LOPT_SMALL_FC_LOPT)
-    apply_strict_kernel<LOPT_SMALL_FC_LOPT><<<P.n_apply_items, kStrictThreads, 0, s>>>(P);
+    apply_strict_kernel<LOPT_SMALL_FC_LOPT><<<P.n_apply_items, kStrictApplyThreads, 0, s>>>(P);
   else
-    apply_strict_kernel<LOPT_VELO_MLP><<<P.n_apply_items, kStrictThreads, 0, s>>>(P);
+    apply_strict_kernel<LOPT_VELO_MLP><<<P.n_apply_items, kStrictApplyThreads, 0, s>>>(P);
 }
 
 void launch_maxabs_reduce(const DevicePlan &P, cudaStream_t s) {
