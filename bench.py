@@ -234,6 +234,22 @@ def time_device(opt, params, grads, steps, warmup, world):
         phases.setdefault(name, []).append(a.elapsed_time(b))
     opt.phase_events = None
     per_step = sorted(marks[k].elapsed_time(marks[k + 1]) for k in range(steps))
+    if world > 1 and hasattr(opt, "set_exchange"):
+        # the same step without the parameter exchange
+        opt.set_exchange(False)
+        for _ in range(2):
+            opt.step(**kw)
+        torch.cuda.synchronize()
+        barrier(world)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(steps):
+            opt.step(**kw)
+        s1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+        opt.set_exchange(True)
+        phases["_no_exchange_ms"] = max_over_ranks(s0.elapsed_time(s1), world) / steps
     q = lambda f: per_step[min(len(per_step) - 1, int(f * (len(per_step) - 1) + 0.5))]  # noqa: E731
     phases["_step_quantiles"] = [q(0.1), q(0.5), q(0.9)]
     launches = sum(pl.launches_last_step() for pl in opt.plans())
@@ -405,6 +421,7 @@ def main():
     local_params = sum(pl.local_elements() for pl in opt.plans())
     achieved = ALGO_BYTES_PER_PARAM * local_params / (apply_ms / 1e3) / 1e9
     quant = phases.pop("_step_quantiles", None)
+    no_exchange_ms = phases.pop("_no_exchange_ms", None)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": None, "kernel": "apply (phase 2)",
                 "peak_source": peak_kind, "frac_vs_8tbs_spec": achieved / 8000.0,
@@ -452,6 +469,7 @@ def main():
                 "value": n_params * args.steps / (vms / 1e3) / 1e9, "unit": "Gparams/s",
                 "ms_per_step": vms / args.steps,
                 "step_ms_p10_p50_p90": vph.pop("_step_quantiles", None),
+                "ms_per_step_without_param_exchange": vph.pop("_no_exchange_ms", None),
                 "phase_ms": {k: statistics.mean(v) for k, v in vph.items()}}
 
     # context: the same parameters stepped by torch's fused
@@ -490,6 +508,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True,
             "step_ms_p10_p50_p90": quant,
+            "ms_per_step_without_param_exchange": no_exchange_ms,
             "scaling": "strong" if world > 1 else "none", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": args.workload, "feature_set": args.feature_set,

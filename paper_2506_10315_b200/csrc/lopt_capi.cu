@@ -40,7 +40,16 @@ namespace {
 
 constexpr int64_t kStrictStatChunk = 8192;
 constexpr int64_t kStrictApplyChunk = 4096;
-constexpr int64_t kFactorTileElems = 131072;   // 256 rows x 512 columns per CTA
+// elements per factor CTA (rows x <=512 columns); LOPT_FACTOR_TILE overrides
+// it for tuning sweeps
+int64_t factor_tile_elems() {
+  static const int64_t v = [] {
+    const char *e = getenv("LOPT_FACTOR_TILE");
+    const long long x = e ? atoll(e) : 0;
+    return x >= 512 ? (int64_t)x : (int64_t)131072;
+  }();
+  return v;
+}
 
 struct Region {
   size_t off = 0, bytes = 0;
@@ -130,17 +139,17 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
     if (!cfg->state_advanced) {
       if (t.n == 1) {
         d.nstrips = 1;
-        d.nrowblocks = (int32_t)((t.m + kFactorTileElems - 1) / kFactorTileElems);
+        d.nrowblocks = (int32_t)((t.m + factor_tile_elems() - 1) / factor_tile_elems());
         for (int rb = 0; rb < d.nrowblocks; rb++) {
           // row blocks outside this call's element range keep zero partials
-          const int64_t r0 = rb * kFactorTileElems, r1 = std::min<int64_t>(t.m, r0 + kFactorTileElems);
+          const int64_t r0 = rb * factor_tile_elems(), r1 = std::min<int64_t>(t.m, r0 + factor_tile_elems());
           if (r1 <= t.lo || r0 >= t.hi) continue;
           FactorItem it{};
           it.tensor = j;
           it.strip = 0;
           it.rowblock = rb;
-          it.a0 = rb * kFactorTileElems;
-          it.a1 = std::min<int64_t>(t.m, it.a0 + kFactorTileElems);
+          it.a0 = rb * factor_tile_elems();
+          it.a1 = std::min<int64_t>(t.m, it.a0 + factor_tile_elems());
           it.b0 = 0;
           it.b1 = 1;
           p->fitems.push_back(it);
@@ -149,7 +158,7 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
         const int64_t strip = factor_strip_cols();
         d.nstrips = (int32_t)((t.n + strip - 1) / strip);
         const int64_t width = std::min<int64_t>(t.n, strip);
-        int64_t R = kFactorTileElems / width;
+        int64_t R = factor_tile_elems() / width;
         R = std::max<int64_t>(8, (R + 7) / 8 * 8);
         d.nrowblocks = (int32_t)((t.m + R - 1) / R);
         for (int rb = 0; rb < d.nrowblocks; rb++)

@@ -277,13 +277,27 @@ __global__ void __launch_bounds__(kFastStatThreads, 4) stats_fast_kernel(DeviceP
 
 // Per-tensor sums: item partials (fixed order) + broadcast closed forms +
 // time columns (count * tf^2).  Writes the all-reducible sumsq block.
-__global__ void stats_reduce_fast_kernel(DevicePlan P) {
+__global__ void __launch_bounds__(256) stats_reduce_fast_kernel(DevicePlan P) {
+  // warp w sums items w, w+8, ... (lanes over features), then the 8 warp
+  // partials are added in warp order: a fixed order, 8 short dependent chains
+  // instead of one chain as long as the tensor's item count
+  constexpr int kWarps = 8;
+  __shared__ double part[kWarps][kMaxFeat];
   const int j = blockIdx.x;
   const TensorDesc T = P.tensors[j];
   const int D = d_feat(P.kind);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = lane; k < D; k += 32) {
+    double s = 0.0;
+    for (int i = warp; i < T.stat_items; i += kWarps)
+      s += P.stat_part[(int64_t)(T.stat_item0 + i) * D + k];
+    part[warp][k] = s;
+  }
+  __syncthreads();
   for (int k = threadIdx.x; k < D; k += blockDim.x) {
     double s = 0.0;
-    for (int i = 0; i < T.stat_items; i++) s += P.stat_part[(int64_t)(T.stat_item0 + i) * D + k];
+#pragma unroll
+    for (int w = 0; w < kWarps; w++) s += part[w][k];
     s += P.bcsum[(int64_t)j * D + k];
     if (P.kind == LOPT_SMALL_FC_LOPT && k >= 26 && k < 37) {
       const double tf = (double)P.step->tf[k - 26];
@@ -312,7 +326,7 @@ void launch_fast_stats(const DevicePlan &P, cudaStream_t s) {
     else
       stats_fast_kernel<LOPT_VELO_MLP><<<P.n_stat_items, kFastStatThreads, 0, s>>>(P);
   }
-  stats_reduce_fast_kernel<<<P.count, 64, 0, s>>>(P);
+  stats_reduce_fast_kernel<<<P.count, 256, 0, s>>>(P);
 }
 
 void launch_tc_apply(const DevicePlan &P, cudaStream_t s);

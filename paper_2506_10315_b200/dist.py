@@ -89,6 +89,7 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         if gather not in ("nccl", "p2p"):
             raise ValueError(f"unknown gather {gather!r}")
         self.gather = gather
+        self.exchange = True
         ps = self.param_groups[0]["params"]
         sizes = [p.numel() for p in ps]
         ranges, S, padded = flat_shard_ranges(sizes, self.world, self.rank)
@@ -107,7 +108,8 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
             dist.all_gather_object(handles, reduce_tensor(self.flat), group=self.pg)
             self._peers = [fn(*args) for r, (fn, args) in enumerate(handles) if r != self.rank]
             base = self.flat.data_ptr()
-            self.set_peer_copies([q.data_ptr() - base for q in self._peers])
+            self._peer_offsets = [q.data_ptr() - base for q in self._peers]
+            self.set_peer_copies(self._peer_offsets)
         else:
             self.flat = torch.zeros(padded, dtype=torch.float32, device=dev)
         off = 0
@@ -180,12 +182,22 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         if self._after_stats is not None:
             timed("hypernet", lambda: self._after_stats(gi, plan, params))
         timed("apply", plan.apply)
+        if not self.exchange:
+            return
         if self._peers is not None:
             # the peers' stores into this arena happened inside their apply
             # kernels; one cross-rank barrier orders them before any read
             timed("param_gather", self._peer_barrier)
         else:
             timed("param_gather", self._gather)
+
+    def set_exchange(self, on: bool):
+        """Diagnostics (step time with and without the
+        all-gather): off, each rank updates only its own slice and the
+        replicas go stale.  Turn it back on before relying on the parameters."""
+        self.exchange = bool(on)
+        if self._peers is not None:
+            self.set_peer_copies(self._peer_offsets if on else [])
 
     def _nccl(self) -> bool:
         return dist.get_backend(self.pg) == "nccl"

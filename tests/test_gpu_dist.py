@@ -32,7 +32,7 @@ def _init(seed=0):
     return init, grads
 
 
-def _worker(rank, world, port, mode, fs, q, gather="nccl"):
+def _worker(rank, world, port, mode, fs, q, gather="nccl", exchange_off_last=False):
     import sys
     import traceback
 
@@ -52,13 +52,18 @@ def _worker(rank, world, port, mode, fs, q, gather="nccl"):
         params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
         opt = ShardedLearnedOptimizer(params, feature_set=fs, mode=mode, weight_decay=0.01,
                                       gather=gather)
-        for gs in grads:
+        for k, gs in enumerate(grads):
             for p, g in zip(params, gs):
                 p.grad = torch.from_numpy(g).cuda()
+            if exchange_off_last and k == len(grads) - 1:
+                opt.set_exchange(False)
             opt.step()
         torch.cuda.synchronize()
         out = [p.detach().cpu().numpy().copy() for p in params]
-        q.put((rank, out, opt.local_state_bytes()))
+        if exchange_off_last:
+            q.put((rank, out, list(opt.ranges)))
+        else:
+            q.put((rank, out, opt.local_state_bytes()))
         dist.destroy_process_group()
     except Exception:
         q.put((rank, traceback.format_exc(), 0))
@@ -108,3 +113,45 @@ def test_sharded_equals_single_gpu(mode, fs, gather):
             else:
                 err = np.abs(a.astype(np.float64) - b) / (1 + np.abs(b))
                 assert err.max() <= 1e-6, err.max()
+
+
+@pytest.mark.parametrize("gather", ["nccl", "p2p"])
+def test_exchange_off_updates_only_own_slice(gather):
+    """set_exchange(False) (bench.py's without-all-gather timing, SURVEY.md
+    §8(e)): a rank's own element range advances, the rest of its replica
+    keeps the previous step's values."""
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_2506_10315_b200 as P
+
+    init, grads = _init()
+    params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    opt = P.LearnedOptimizer(params, mode="fast", weight_decay=0.01)
+    snaps = []
+    for gs in grads:
+        for p, g in zip(params, gs):
+            p.grad = torch.from_numpy(g).cuda()
+        opt.step()
+        snaps.append([p.detach().cpu().numpy().reshape(-1).copy() for p in params])
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, "fast", "small_fc_lopt", q, gather,
+                                               True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, out, ranges in res:
+        assert not isinstance(out, str), out
+        for a, new, old, (lo, hi) in zip(out, snaps[-1], snaps[-2], ranges):
+            a = a.reshape(-1).astype(np.float64)
+            own = np.zeros(a.size, bool)
+            own[lo:hi] = True
+            err = np.abs(a[own] - new[own]) / (1 + np.abs(new[own]))
+            assert own.sum() == 0 or err.max() <= 1e-6
+            err = np.abs(a[~own] - old[~own]) / (1 + np.abs(old[~own]))
+            assert (~own).sum() == 0 or err.max() <= 1e-6
