@@ -17,6 +17,7 @@ lives in optim.py.
 from __future__ import annotations
 
 import ctypes
+from typing import NamedTuple
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -302,25 +303,76 @@ def _check_step_inputs(W, g, state, weights, spec):
 
 def _engine_plan(W, g, state, weights, spec, mode, lo=None, hi=None):
     m, n = state.shape
-    slot = Slot(theta=W.reshape(-1), grad=g.reshape(-1).contiguous(), state=state.quad,
-                r=state.r, c=state.c, m=m, n=n, lo=0 if lo is None else lo,
-                hi=m * n if hi is None else hi)
+    lo = 0 if lo is None else int(lo)
+    hi = m * n if hi is None else int(hi)
+    if not 0 <= lo <= hi <= m * n:
+        raise EngineError(f"element range [{lo}, {hi}) outside a {m}x{n} tensor")
+    slot = Slot(theta=W.reshape(-1), grad=g.reshape(-1).contiguous(), state=state.quad[lo:hi],
+                r=state.r, c=state.c, m=m, n=n, lo=lo, hi=hi)
     return StepPlan([slot], spec, weights, mode=mode, state_advanced=True)
 
 
-def fused_stats(W, g, state: DeviceOptState, spec=None, workers: int = 1, mode="strict"):
-    """engine.py:619-654 pass 1.  Returns (sumsq float64 CUDA tensor, count).
-    `workers` only partitions the reference's f64 reduction; the device
-    reduction order is fixed by the plan instead."""
+class FeatureStats(NamedTuple):
+    """features.py:107-118: column sums of squared features (f64, here a CUDA
+    tensor) and the element count behind them.  Unpacks as (sumsq, count)."""
+
+    sumsq: torch.Tensor
+    count: int
+
+
+def fused_stats(W, g, state: DeviceOptState, spec=None, workers: int = 1, tracker=None,
+                lo: int | None = None, hi: int | None = None, mode="strict") -> FeatureStats:
+    """engine.py:619-654 pass 1 over the element range [lo, hi) (default: the
+    whole tensor).  `workers` and `tracker` are accepted for signature parity:
+    `workers` only partitions the reference's f64 reduction and the device
+    reduction order is fixed by the plan; device scratch is the plan's own
+    workspace (lopt_workspace_bytes), not a tracked host allocation.  Range
+    stats add: the sharded step all-reduces them (distsim.py:489-490)."""
     spec = spec or small_fc_lopt_spec()
     from .weights import zero_weights
 
-    plan = _engine_plan(W.clone(), g, state, zero_weights(spec.d_feat), spec, mode)
+    plan = _engine_plan(W.detach().clone(), g.detach(), state, zero_weights(spec.d_feat), spec,
+                        mode, lo, hi)
     plan.set_step(1.0, 0.0, state.t)
     plan.factor_partials()
     plan.factor_finalize()
     plan.feature_stats()
-    return plan.stat_sums()[0].clone(), W.numel()
+    count = plan.slots[0].hi - plan.slots[0].lo
+    return FeatureStats(plan.stat_sums()[0].clone(), count)
+
+
+def fused_apply(W, g, state: DeviceOptState, weights: LoptWeights, spec, stats, out,
+                lr: float = 1.0, tracker=None, lo: int | None = None, hi: int | None = None,
+                mode="strict") -> float:
+    """engine.py:657-710 pass 2 over [lo, hi): features normalized by the
+    given whole-tensor `stats` (FeatureStats or a (sumsq, count) pair; the
+    scale uses the tensor's element count, as the fold at engine.py:686
+    does), MLP, update written into out[lo:hi] (a CUDA tensor shaped like W;
+    the rest of `out` is not touched).  Returns max |update| over the range.
+    The state must already be advanced for g."""
+    spec = spec or small_fc_lopt_spec()
+    _check_step_inputs(W, g, state, weights, spec)
+    if tuple(out.shape) != tuple(W.shape) or not out.is_contiguous():
+        raise EngineError(f"out must be a contiguous tensor shaped {tuple(W.shape)}")
+    sumsq, count = (stats[0], stats[1]) if isinstance(stats, tuple) else (stats.sumsq, stats.count)
+    m, n = state.shape
+    if int(count) != m * n:
+        # the device folds 1/sqrt(sumsq/(m*n) + eps) into W1 (lopt_fast.cu /
+        # lopt_strict.cu); merged stats always carry the whole-tensor count
+        raise EngineError(f"stats cover {int(count)} elements; the apply pass needs the "
+                          f"whole tensor's ({m * n}) -- merge the range stats first")
+    lo_ = 0 if lo is None else int(lo)
+    hi_ = m * n if hi is None else int(hi)
+    flat = out.view(-1)
+    flat[lo_:hi_].copy_(W.detach().reshape(-1)[lo_:hi_])
+    plan = _engine_plan(out, g.detach(), state, weights, spec, mode, lo, hi)
+    plan.set_step(lr, 0.0, state.t)
+    plan.factor_partials()
+    plan.factor_finalize()
+    plan.stat_sums()[0].copy_(torch.as_tensor(sumsq, dtype=torch.float64))
+    plan.apply()
+    _, mx = plan.status()
+    return float(mx[0])
 
 
 def step_fused(W, g, state: DeviceOptState, weights: LoptWeights, spec=None, lr: float = 1.0,

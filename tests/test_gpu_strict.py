@@ -284,3 +284,51 @@ def test_hundred_steps_relative_l2_vs_oracle(P, oracle):
         quad = opt.state[p]["quad"].cpu().numpy()
         assert quad[:, 3].tobytes() == s.V.reshape(-1).tobytes()
         assert quad[:, 0].tobytes() == s.M[0].reshape(-1).tobytes()
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+@pytest.mark.parametrize("spec_name", ["small_fc_lopt", "velo_mlp"])
+@pytest.mark.parametrize("shape", [(33, 70), (17, 129), (1, 130), (64, 64)])
+def test_range_operator_pair_matches_whole_tensor(P, oracle, spec_name, shape, mode):
+    """engine.py:619-710 range-level pair as the sharded step uses it
+    (distsim.py:489-490,513-514): fused_stats over [0,k) and [k,mn) add up to
+    the whole-tensor stats (acceptance 9), and fused_apply over the two ranges
+    with the merged stats writes exactly what step_fused does (itself pinned
+    bitwise to the reference above) -- bit for bit."""
+    import torch
+
+    O = oracle
+    G = load_golden("engine_cases.npz")
+    m, n = shape
+    key = f"{spec_name}/{m}x{n}"
+    s = _golden_state(O, G, key, m, n)
+    spec = P.spec_by_name(spec_name)
+    W = torch.from_numpy(G[key + "/W"]).cuda()
+    g = torch.from_numpy(G[key + "/g"]).cuda()
+    w = P.random_weights(spec.d_feat, seed=int(G[key + "/wseed"][0]))
+    mn = m * n
+    k = mn // 3
+    whole = P.fused_stats(W, g, _dev_state(P, O, s), spec, mode=mode)
+    a = P.fused_stats(W, g, _dev_state(P, O, s), spec, lo=0, hi=k, mode=mode)
+    b = P.fused_stats(W, g, _dev_state(P, O, s), spec, lo=k, hi=mn, mode=mode)
+    assert a.count + b.count == whole.count == mn
+    merged = a.sumsq + b.sumsq
+    # strict: f64 sums of exact squares; fast: f32 per-thread partials (the
+    # reference's own additivity bound is 1e-6, acceptance 9)
+    np.testing.assert_allclose(merged.cpu().numpy(), whole.sumsq.cpu().numpy(),
+                               rtol=1e-12 if mode == "strict" else 1e-6)
+    ref, _ = P.step_fused(W, g, _dev_state(P, O, s), w, spec, lr=0.3, mode=mode)
+    out = torch.full_like(W, float("nan"))
+    st = _dev_state(P, O, s)
+    mx0 = P.fused_apply(W, g, st, w, spec, (merged, mn), out, lr=0.3, lo=0, hi=k, mode=mode)
+    assert torch.isnan(out.view(-1)[k:]).all()
+    mx1 = P.fused_apply(W, g, st, w, spec, P.FeatureStats(merged, mn), out, lr=0.3,
+                        lo=k, hi=mn, mode=mode)
+    if mode == "strict":
+        assert out.cpu().numpy().tobytes() == ref.cpu().numpy().tobytes()
+    else:   # merged range sums may differ from the whole-tensor sums in the last f64 bits
+        a_, r_ = out.cpu().numpy().astype(np.float64), ref.cpu().numpy()
+        assert (np.abs(a_ - r_) / (1 + np.abs(r_))).max() <= 1e-7
+    assert max(mx0, mx1) > 0
+    with pytest.raises(P.EngineError):
+        P.fused_apply(W, g, st, w, spec, a, out, lr=0.3, lo=0, hi=k, mode=mode)
