@@ -721,6 +721,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
         for (int q = 0; q < n_peers; q++)
           *reinterpret_cast<float *>(reinterpret_cast<char *>(tp) + P.peer_delta[q]) = out;
       }
+      if (warp == kWarpC) trace(P, i, 7);
       rc.next();
       sc.next();
     }

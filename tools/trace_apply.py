@@ -29,13 +29,15 @@ L = _lib.lib()
 buf = (ctypes.c_longlong * (64 * 8))()
 L.lopt_debug_apply_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 assert L.lopt_debug_apply_trace(ctypes.addressof(buf), 64 * 8) == 0
-t = np.array(buf[:], dtype=np.int64).reshape(64, 8)[:, :7]
-t = t - t[0, 0]
-names = ["prod", "A_in", "A_out", "mma1", "B_in", "mma2", "C_in"]
+t = np.array(buf[:], dtype=np.int64).reshape(64, 8)
+ev = t[0::2]          # the first warp of each role's warpgroup 0 records: even tiles
+ev = ev - ev[0, 0]
+names = ["prod", "A_in", "A_out", "mma1", "B_in", "mma2", "C_in", "C_end"]
 print("tile " + " ".join(f"{n:>8s}" for n in names))
-for i in range(64):
-    print(f"{i:4d} " + " ".join(f"{v:8d}" for v in t[i]))
-d = np.diff(t[8:, :], axis=0).mean(axis=0)
-print("mean per-tile spacing (tiles 8..63):", " ".join(f"{n}={v:.0f}" for n, v in zip(names, d)))
-lat = (t[8:, 1:] - t[8:, :-1]).mean(axis=0)
+for k in range(ev.shape[0]):
+    print(f"{2 * k:4d} " + " ".join(f"{v:8d}" for v in ev[k]))
+s_ = ev[4:]
+print("cycles per tile (even-tile spacing / 2):",
+      " ".join(f"{n}={v:.0f}" for n, v in zip(names, np.diff(s_, axis=0).mean(axis=0) / 2)))
+lat = (s_[:, 1:] - s_[:, :-1]).mean(axis=0)
 print("mean stage latency:", " ".join(f"{names[k]}->{names[k+1]}={v:.0f}" for k, v in enumerate(lat)))
