@@ -2,24 +2,28 @@
 (instructions per element) and the hottest stall lines.
 
     python tools/ncu_summary.py gpurun_out/prof_apply_v6.ncu-rep [elements]
+    LOPT_NCU_KERNEL=apply_tc python tools/ncu_summary.py <multi-kernel report>
 """
 import collections
 import csv
 import io
+import os
 import subprocess
 import sys
 
 rep = sys.argv[1]
 elems = float(sys.argv[2]) if len(sys.argv) > 2 else 86567656.0
+# LOPT_NCU_KERNEL=regex selects one kernel of a multi-kernel report
+KF = ['-k', 'regex:' + os.environ['LOPT_NCU_KERNEL']] if os.environ.get('LOPT_NCU_KERNEL') else []
 want = ['Duration', 'DRAM Throughput', 'Executed Ipc Active', 'Issue Slots Busy', 'No Eligible',
         'Active Warps Per Scheduler', 'Eligible Warps Per Scheduler',
         'Warp Cycles Per Issued Instruction', 'Issued Instructions', 'Registers Per Thread',
         'L1/TEX Hit Rate', 'L2 Hit Rate', 'SM Frequency']
-det = subprocess.run(['ncu', '-i', rep, '--page', 'details', '--csv'], capture_output=True, text=True).stdout
+det = subprocess.run(['ncu', '-i', rep] + KF + [ '--page', 'details', '--csv'], capture_output=True, text=True).stdout
 for r in csv.reader(io.StringIO(det)):
     if len(r) > 14 and r[12] in want:
         print(f"{r[12]:40s} {r[14]} {r[13]}")
-raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+raw = subprocess.run(['ncu', '-i', rep] + KF + [ '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 if len(rows) > 2:
     hdr, units, vals = rows[0], rows[1], rows[2]
@@ -27,7 +31,7 @@ if len(rows) > 2:
         if key in hdr:
             i = hdr.index(key)
             print(f"{key:40s} {vals[i]} {units[i]}")
-src = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'sass'],
+src = subprocess.run(['ncu', '-i', rep] + KF + [ '--page', 'source', '--csv', '--print-source', 'sass'],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hdr, data = rows[1], rows[2:]
