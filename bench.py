@@ -161,7 +161,7 @@ def make_model(workload, device, seed=0):
     return params, grads
 
 
-def build_optimizer(params, feature_set, mode, world):
+def build_optimizer(params, feature_set, mode, world, strategy="range"):
     """feature_set "velo" is the full VeLO optimizer (VELO_MLP features + the
     per-tensor LSTM hypernetwork mixing a bank of MLPs); "small_fc_lopt" and
     "velo_mlp" are the single-MLP learned optimizers."""
@@ -173,10 +173,11 @@ def build_optimizer(params, feature_set, mode, world):
             from paper_2506_10315_b200.dist import ShardedVeLO
 
             try:
-                return ShardedVeLO(params, mode=mode, check_errors=False, gather=gather)
+                return ShardedVeLO(params, mode=mode, check_errors=False, gather=gather,
+                                   strategy=strategy)
             except Exception as e:  # noqa: BLE001
                 print(f"bench: p2p gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
-                return ShardedVeLO(params, mode=mode, check_errors=False)
+                return ShardedVeLO(params, mode=mode, check_errors=False, strategy=strategy)
         from paper_2506_10315_b200.velo import VeLO_CUDA
 
         return VeLO_CUDA(params, mode=mode, check_errors=False)
@@ -185,11 +186,11 @@ def build_optimizer(params, feature_set, mode, world):
 
         try:
             return ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
-                                           check_errors=False, gather=gather)
+                                           check_errors=False, gather=gather, strategy=strategy)
         except Exception as e:  # noqa: BLE001
             print(f"bench: p2p gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
             return ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
-                                           check_errors=False)
+                                           check_errors=False, strategy=strategy)
     from paper_2506_10315_b200 import LearnedOptimizer
 
     return LearnedOptimizer(params, feature_set=feature_set, mode=mode, check_errors=False)
@@ -391,6 +392,9 @@ def main():
                     help="fast (tensor-core product path, fp32 tolerance) or strict (bitwise)")
     ap.add_argument("--cpu-budget", type=int, default=0,
                     help="params in the bounded CPU sample (0: the whole workload)")
+    ap.add_argument("--strategy", default=os.environ.get("LOPT_SHARD_STRATEGY", "range"),
+                    choices=["range", "owner"],
+                    help="N>1: element ranges (REDUCE_SCATTER) or whole tensors per owner (FSDP_A2A)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-velo", action="store_true")
@@ -411,7 +415,7 @@ def main():
     dev = torch.device("cuda", torch.cuda.current_device())
     params, grads = make_model(args.workload, dev, seed=0)
 
-    opt = build_optimizer(params, args.feature_set, args.mode, world)
+    opt = build_optimizer(params, args.feature_set, args.mode, world, args.strategy)
     gather_used = getattr(opt, "gather", "nccl")
     clk = ClockSampler(torch.cuda.current_device())
     clk.__enter__()   # sampled through the timed steps, the phase pass and the e2e run
@@ -462,7 +466,7 @@ def main():
         del opt
         torch.cuda.empty_cache()
         params, grads = make_model(args.workload, dev, seed=0)
-        vopt = build_optimizer(params, "velo", args.mode, world)
+        vopt = build_optimizer(params, "velo", args.mode, world, args.strategy)
         vms, vph, _ = time_device(vopt, params, grads, args.steps, args.warmup, world)
         velo = {"optimizer": "VeLO_CUDA (VELO_MLP features + per-tensor LSTM hypernetwork, "
                              "bank of 4 MLPs)",
@@ -513,7 +517,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": args.workload, "feature_set": args.feature_set,
                        "mode": args.mode, "tensors": n_tensors, "params": n_params,
-                       "parallelism": (f"element-sharded x{world}, param exchange "
+                       "parallelism": (("element-sharded" if args.strategy == "range" else
+                                        "tensor-owner-sharded") + f" x{world}, param exchange "
                                        f"{gather_used}") if world > 1 else "single",
                        "l2": f"inputs larger than L2 (each f32 array {n_params * 4 / 1e6:.0f} MB "
                              f"> 126 MB)"},

@@ -1,9 +1,7 @@
 """Data-parallel sharded optimizer step over torch.distributed (NCCL on GPUs).
 
-The reference simulates three strategies in distsim.py; this module runs the
-element-range one for real (REDUCE_SCATTER, distsim.py:403-534) and keeps the
-whole-tensor ownership plan of FSDP_A2A (distsim.py:99-123) available as a
-partition helper:
+The reference simulates three strategies in distsim.py; this module runs two
+of them for real.  strategy="range" is REDUCE_SCATTER (distsim.py:403-534):
 
   * parameters are flattened into one arena (like ZeRO / FSDP flat params) and
     rank r owns the contiguous slice [r*S, (r+1)*S) of it; for every tensor
@@ -21,6 +19,14 @@ partition helper:
 
 Merging f64 partials reproduces the single-device f32 factors and scales
 (SURVEY.md Appendix A), so the sharded step matches the 1-GPU step.
+
+strategy="owner" is FSDP_A2A (distsim.py:536-595): every tensor is stepped
+whole by one owner (greedy largest-first, distsim.py:109-118), so there is no
+factor or stats merge -- only the one-word non-finite-gradient flag is
+all-reduced, keeping the step all-or-nothing across ranks.  The arena is laid
+out owner by owner (rank r's tensors in [r*S, (r+1)*S)), so the same in-place
+all-gather (or the fused peer stores) redistributes the parameters.  Balance
+is limited by the largest tensor.
 """
 
 from __future__ import annotations
@@ -61,6 +67,24 @@ def flat_shard_ranges(sizes, world: int, rank: int):
     return out, S, padded
 
 
+def owner_layout(sizes, owner, world: int, rank: int):
+    """Arena layout of the ownership strategy: rank r's tensors (in tensor
+    order) packed from r*S, S = the largest owner total rounded up to 128.
+    Returns (ranges, offsets, S, padded): this rank steps (0, n) of the
+    tensors it owns and the empty range of the others."""
+    load = [0] * world
+    for n, w in zip(sizes, owner):
+        load[w] += n
+    S = max(128, (max(load) + 127) // 128 * 128)
+    cursor = [r * S for r in range(world)]
+    offsets, ranges = [], []
+    for n, w in zip(sizes, owner):
+        offsets.append(cursor[w])
+        cursor[w] += n
+        ranges.append((0, n) if w == rank else (0, 0))
+    return ranges, offsets, S, world * S
+
+
 def owner_plan(sizes, workers: int):
     """distsim.py:109-118 FSDP_A2A ownership: greedy largest-first."""
     order = sorted(range(len(sizes)), key=lambda j: -sizes[j])
@@ -79,7 +103,8 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
     ranks at construction; gradients are expected to be already reduced
     (e.g. DDP), of which each rank reads only its own slice."""
 
-    def __init__(self, params, *args, process_group=None, gather: str = "nccl", **kw):
+    def __init__(self, params, *args, process_group=None, gather: str = "nccl",
+                 strategy: str = "range", **kw):
         super().__init__(params, *args, **kw)
         self.pg = process_group
         self.world = dist.get_world_size(self.pg)
@@ -88,11 +113,20 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
             raise ValueError("the sharded step supports one parameter group")
         if gather not in ("nccl", "p2p"):
             raise ValueError(f"unknown gather {gather!r}")
+        if strategy not in ("range", "owner"):
+            raise ValueError(f"unknown strategy {strategy!r}")
         self.gather = gather
+        self.strategy = strategy
         self.exchange = True
         ps = self.param_groups[0]["params"]
         sizes = [p.numel() for p in ps]
-        ranges, S, padded = flat_shard_ranges(sizes, self.world, self.rank)
+        if strategy == "range":
+            ranges, S, padded = flat_shard_ranges(sizes, self.world, self.rank)
+            offsets = list(np.cumsum([0] + sizes[:-1]))
+        else:
+            self.owner = owner_plan(sizes, self.world)
+            ranges, offsets, S, padded = owner_layout(sizes, self.owner, self.world, self.rank)
+        self.offsets = [int(o) for o in offsets]
         dev = ps[0].device
         self._peers = None
         if gather == "p2p":
@@ -112,11 +146,9 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
             self.set_peer_copies(self._peer_offsets)
         else:
             self.flat = torch.zeros(padded, dtype=torch.float32, device=dev)
-        off = 0
-        for p, n in zip(ps, sizes):
+        for p, n, off in zip(ps, sizes, self.offsets):
             self.flat[off:off + n].copy_(p.data.view(-1))
             p.data = self.flat[off:off + n].view(p.shape)
-            off += n
         self.slice_len = S
         self.ranges = ranges
         for p, (lo, hi) in zip(ps, ranges):
@@ -138,13 +170,11 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         if getattr(self, "_flat_grad", None) is None:
             ps = self.param_groups[0]["params"]
             self._flat_grad = torch.zeros_like(self.flat)
-            off = 0
-            for p in ps:
+            for p, off in zip(ps, self.offsets):
                 n = p.numel()
                 if p.grad is not None:
                     self._flat_grad[off:off + n].copy_(p.grad.reshape(-1))
                 p.grad = self._flat_grad[off:off + n].view(p.shape)
-                off += n
         return self._flat_grad
 
     def reduce_scatter_grads(self, average: bool = True):
@@ -175,10 +205,16 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         timed = self._timed
         plan.set_step(lr, weight_decay, t)
         timed("factors", plan.factor_partials)
-        timed("factor_merge", lambda: self._all_reduce(plan.factor_sums()))
+        if self.strategy == "range":
+            timed("factor_merge", lambda: self._all_reduce(plan.factor_sums()))
+        else:   # whole tensors: only the abort flag is shared (all-or-nothing step)
+            timed("factor_merge", lambda: self._all_reduce(plan.factor_sums()[-1:]))
         timed("finalize", plan.factor_finalize)
         timed("stats", plan.feature_stats)
-        timed("stats_merge", lambda: self._all_reduce(plan.stat_sums()))
+        if self.strategy == "range" or self._after_stats is not None:
+            # (owner + VeLO: the per-tensor LSTM runs on every rank and needs
+            # every tensor's statistics; 47 KB for ViT-B/16)
+            timed("stats_merge", lambda: self._all_reduce(plan.stat_sums()))
         if self._after_stats is not None:
             timed("hypernet", lambda: self._after_stats(gi, plan, params))
         timed("apply", plan.apply)

@@ -213,3 +213,26 @@ def test_reduce_scatter_grads_gloo_world2():
     mean = np.concatenate([mean, np.zeros(2 * S - mean.size, np.float32)])
     for rank, _, _, sl in res:
         np.testing.assert_allclose(sl, mean[rank * S:(rank + 1) * S], rtol=0, atol=1e-9)
+
+
+def test_owner_layout_partitions_the_arena():
+    """FSDP_A2A ownership (distsim.py:109-118): greedy largest-first owners;
+    the arena puts each owner's tensors in its own slice, disjoint, and every
+    tensor is stepped by exactly one rank."""
+    from paper_2506_10315_b200.dist import owner_layout, owner_plan
+
+    sizes = [2359296, 768, 589824, 3, 1, 2304, 50257 * 1024, 7]
+    for world in (1, 2, 3, 8):
+        owner = owner_plan(sizes, world)
+        loads = [sum(n for n, w in zip(sizes, owner) if w == r) for r in range(world)]
+        assert max(loads) - min(loads) <= max(sizes)
+        seen = np.zeros(world * max(128, (max(loads) + 127) // 128 * 128), np.int32)
+        for rank in range(world):
+            ranges, offsets, S, padded = owner_layout(sizes, owner, world, rank)
+            assert S % 128 == 0 and padded == world * S
+            for n, w, (lo, hi), off in zip(sizes, owner, ranges, offsets):
+                assert (lo, hi) == ((0, n) if w == rank else (0, 0))
+                assert w * S <= off and off + n <= (w + 1) * S
+                if w == rank:
+                    seen[off:off + n] += 1
+        assert seen.max() == 1 and seen.sum() == sum(sizes)

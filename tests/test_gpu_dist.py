@@ -32,7 +32,8 @@ def _init(seed=0):
     return init, grads
 
 
-def _worker(rank, world, port, mode, fs, q, gather="nccl", exchange_off_last=False):
+def _worker(rank, world, port, mode, fs, q, gather="nccl", exchange_off_last=False,
+            strategy="range"):
     import sys
     import traceback
 
@@ -51,7 +52,7 @@ def _worker(rank, world, port, mode, fs, q, gather="nccl", exchange_off_last=Fal
         init, grads = _init()
         params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
         opt = ShardedLearnedOptimizer(params, feature_set=fs, mode=mode, weight_decay=0.01,
-                                      gather=gather)
+                                      gather=gather, strategy=strategy)
         for k, gs in enumerate(grads):
             for p, g in zip(params, gs):
                 p.grad = torch.from_numpy(g).cuda()
@@ -69,15 +70,20 @@ def _worker(rank, world, port, mode, fs, q, gather="nccl", exchange_off_last=Fal
         q.put((rank, traceback.format_exc(), 0))
 
 
-@pytest.mark.parametrize("mode,fs,gather", [("strict", "small_fc_lopt", "nccl"),
-                                            ("fast", "velo_mlp", "nccl"),
-                                            ("fast", "small_fc_lopt", "nccl"),
-                                            ("fast", "small_fc_lopt", "p2p")])
-def test_sharded_equals_single_gpu(mode, fs, gather):
-    """gather="p2p": the parameter arena in symmetric memory, the apply kernel
-    storing every updated parameter into the other rank's mapped arena (the
+@pytest.mark.parametrize("mode,fs,gather,strategy", [
+    ("strict", "small_fc_lopt", "nccl", "range"),
+    ("fast", "velo_mlp", "nccl", "range"),
+    ("fast", "small_fc_lopt", "nccl", "range"),
+    ("fast", "small_fc_lopt", "p2p", "range"),
+    ("strict", "small_fc_lopt", "nccl", "owner"),
+    ("strict", "velo_mlp", "nccl", "owner"),
+    ("fast", "small_fc_lopt", "p2p", "owner")])
+def test_sharded_equals_single_gpu(mode, fs, gather, strategy):
+    """gather="p2p": the parameter arena mapped into the other rank (CUDA
+    IPC), the apply kernel storing every updated parameter into it (the
     NVLink path; here both ranks map one device), one barrier instead of the
-    all-gather."""
+    all-gather.  strategy="owner": whole tensors per rank (FSDP_A2A), no
+    factor/stats merge -- bitwise in strict mode like the range split."""
     import torch
     import torch.multiprocessing as mp
 
@@ -96,7 +102,8 @@ def test_sharded_equals_single_gpu(mode, fs, gather):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, fs, q, gather)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, fs, q, gather, False, strategy))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
@@ -105,8 +112,11 @@ def test_sharded_equals_single_gpu(mode, fs, gather):
     for rank, out, state_bytes in res:
         assert not isinstance(out, str), out
         # optimizer state is sharded: each rank holds about half (slices are
-        # rounded up to whole 128-element tiles)
-        assert state_bytes <= full_state // 2 + 16 * 128 + 4 * 4 * len(SHAPES)
+        # rounded up to whole 128-element tiles; whole tensors per owner)
+        bound = full_state // 2 + 16 * 128 + 4 * 4 * len(SHAPES)
+        if strategy == "owner":
+            bound = full_state // 2 + 16 * max(int(np.prod(s)) for s in SHAPES) + 16 * len(SHAPES)
+        assert state_bytes <= bound
         for a, b in zip(out, single):
             if mode == "strict":
                 assert a.tobytes() == b.tobytes()
