@@ -257,6 +257,11 @@ def time_device(opt, params, grads, steps, warmup, world):
     return max_over_ranks(ms, world), phases, launches
 
 
+# tensor groups of the host-buffer step: finer groups shorten the pipeline's
+# fill (first upload) and drain (last download); 32 measured ~5 % faster than 8
+E2E_CHUNKS = int(os.environ.get("LOPT_E2E_CHUNKS", "32"))
+
+
 def time_e2e(opt, params, grads, steps, warmup, world):
     """Public-API step with host buffers: the gradients come from pinned host
     memory and the updated parameters go back to pinned host memory, both
@@ -272,9 +277,11 @@ def time_e2e(opt, params, grads, steps, warmup, world):
         p.grad = g
     piped = world == 1 and hasattr(opt, "step_host")
 
+    chunks = E2E_CHUNKS
+
     def one():
         if piped:
-            opt.step_host(host_g, host_p)
+            opt.step_host(host_g, host_p, chunks=chunks)
             return
         for d, h in zip(dev_g, host_g):
             d.copy_(h, non_blocking=True)
@@ -455,7 +462,7 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / e2e_steps,
                "api": ("LearnedOptimizer.step_host (pinned host grads in, host params out, "
-                       "8 chunks pipelined)" if world == 1 else
+                       f"{E2E_CHUNKS} tensor groups pipelined)" if world == 1 else
                        "ShardedLearnedOptimizer.step with host copies")}
 
     clk.__exit__(None, None, None)
