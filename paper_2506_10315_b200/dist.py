@@ -67,6 +67,49 @@ def flat_shard_ranges(sizes, world: int, rank: int):
     return out, S, padded
 
 
+def bucketed_layout(sizes, world: int, rank: int, bucket_elems=None, order=None):
+    """Element-range layout with gradient buckets: tensors (in `order`, by
+    default parameter order) are grouped into buckets of at least
+    `bucket_elems` elements (None: one bucket), each bucket is padded to a
+    multiple of 128 * world and cut into `world` equal portions, rank r
+    stepping portion r of every bucket.  A tensor lies in one bucket, so it
+    still gets a single (possibly empty) element range per rank, and each
+    bucket's gradient reduce-scatter / parameter all-gather is one in-place
+    collective on a contiguous arena segment.  With one bucket this is
+    flat_shard_ranges' layout.  Returns (ranges, offsets, buckets, padded),
+    buckets = [(base, portion_len, tensor indices)]."""
+    n = len(sizes)
+    order = list(range(n)) if order is None else [int(j) for j in order]
+    groups = [order]
+    if bucket_elems is not None:
+        groups, cur, acc = [], [], 0
+        for j in order:
+            cur.append(j)
+            acc += sizes[j]
+            if acc >= bucket_elems:
+                groups.append(cur)
+                cur, acc = [], 0
+        if cur:
+            groups.append(cur)
+    unit = world * 128
+    offsets, ranges, buckets = [0] * n, [(0, 0)] * n, []
+    base = 0
+    for tl in groups:
+        tot = sum(sizes[j] for j in tl)
+        seg = max(unit, (tot + unit - 1) // unit * unit)
+        S = seg // world
+        s0, s1 = base + rank * S, base + (rank + 1) * S
+        off = base
+        for j in tl:
+            offsets[j] = off
+            lo, hi = max(off, s0) - off, min(off + sizes[j], s1) - off
+            ranges[j] = (lo, hi) if hi > lo else (0, 0)
+            off += sizes[j]
+        buckets.append((base, S, list(tl)))
+        base += seg
+    return ranges, offsets, buckets, base
+
+
 def owner_layout(sizes, owner, world: int, rank: int):
     """Arena layout of the ownership strategy: rank r's tensors (in tensor
     order) packed from r*S, S = the largest owner total rounded up to 128.
@@ -104,7 +147,7 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
     (e.g. DDP), of which each rank reads only its own slice."""
 
     def __init__(self, params, *args, process_group=None, gather: str = "nccl",
-                 strategy: str = "range", **kw):
+                 strategy: str = "range", bucket_elems=None, **kw):
         super().__init__(params, *args, **kw)
         self.pg = process_group
         self.world = dist.get_world_size(self.pg)
@@ -121,11 +164,18 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         ps = self.param_groups[0]["params"]
         sizes = [p.numel() for p in ps]
         if strategy == "range":
-            ranges, S, padded = flat_shard_ranges(sizes, self.world, self.rank)
-            offsets = list(np.cumsum([0] + sizes[:-1]))
+            # buckets in reverse parameter order: roughly the order backward
+            # produces the gradients (what DDP's bucketing assumes)
+            order = None if bucket_elems is None else list(reversed(range(len(sizes))))
+            ranges, offsets, buckets, padded = bucketed_layout(sizes, self.world, self.rank,
+                                                               bucket_elems, order)
         else:
+            if bucket_elems is not None:
+                raise ValueError("gradient buckets need strategy='range'")
             self.owner = owner_plan(sizes, self.world)
             ranges, offsets, S, padded = owner_layout(sizes, self.owner, self.world, self.rank)
+            buckets = [(0, S, list(range(len(sizes))))]
+        self.buckets = buckets
         self.offsets = [int(o) for o in offsets]
         dev = ps[0].device
         self._peers = None
@@ -149,7 +199,9 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         for p, n, off in zip(ps, sizes, self.offsets):
             self.flat[off:off + n].copy_(p.data.view(-1))
             p.data = self.flat[off:off + n].view(p.shape)
-        self.slice_len = S
+        # single bucket: rank r's slice is [r*S, (r+1)*S) of the whole arena
+        self.slice_len = buckets[0][1] if len(buckets) == 1 else None
+        self._rs_hooks = None
         self.ranges = ranges
         for p, (lo, hi) in zip(ps, ranges):
             st = self.state[p]
@@ -177,24 +229,94 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
                 p.grad = self._flat_grad[off:off + n].view(p.shape)
         return self._flat_grad
 
+    def _bucket_rs(self, b: int, average: bool, async_op: bool):
+        """Reduce-scatter of bucket b's gradient segment into this rank's
+        portion of it (in place).  Returns the NCCL work handle (async_op)."""
+        base, S, _ = self.buckets[b]
+        fg = self._flat_grad
+        seg = fg[base:base + self.world * S]
+        local = seg[self.rank * S:(self.rank + 1) * S]
+        if self._nccl():
+            op = dist.ReduceOp.AVG if average else dist.ReduceOp.SUM
+            return dist.reduce_scatter_tensor(local, seg, op=op, group=self.pg, async_op=async_op)
+        # gloo has no reduce-scatter: all-reduce through the host, keep the portion
+        h = seg.cpu()
+        dist.all_reduce(h, group=self.pg)
+        local.copy_(h[self.rank * S:(self.rank + 1) * S].to(fg.device))
+        if average:
+            local.div_(self.world)
+        return None
+
     def reduce_scatter_grads(self, average: bool = True):
         """Sum (or average) the ranks' local gradients so that each rank holds
         the reduced values of its own slice -- all the sharded step reads
         (distsim.py:323-334 mean_grads, restricted to the owned range).  One
-        in-place NCCL reduce-scatter: half the bytes of the all-reduce DDP
-        would otherwise run."""
+        in-place NCCL reduce-scatter per bucket: half the bytes of the
+        all-reduce DDP would otherwise run.  Returns this rank's portion
+        (one bucket) or the list of portions."""
         fg = self.flat_grads()
-        S = self.slice_len
-        local = fg[self.rank * S:(self.rank + 1) * S]
-        if self._nccl():
-            dist.reduce_scatter_tensor(local, fg, group=self.pg)
-        else:   # gloo has no reduce-scatter: all-reduce through the host, keep the slice
-            h = fg.cpu()
-            dist.all_reduce(h, group=self.pg)
-            local.copy_(h[self.rank * S:(self.rank + 1) * S].to(fg.device))
-        if average:
-            local.div_(self.world)
-        return local
+        out = []
+        for b, (base, S, _) in enumerate(self.buckets):
+            self._bucket_rs(b, average, async_op=False)
+            out.append(fg[base + self.rank * S:base + (self.rank + 1) * S])
+        return out[0] if len(out) == 1 else out
+
+    # -- reduce-scatter overlapped with backward (SURVEY.md §8(f) rank 2) -----
+    def overlap_grad_reduce(self, average: bool = True):
+        """Feed the step straight from backward: gradients accumulate into the
+        bucketed gradient arena and, as soon as every gradient of a bucket
+        has been accumulated (post-accumulate-grad hooks), that bucket's
+        reduce-scatter is launched asynchronously, overlapping the rest of
+        backward -- DDP's bucketed all-reduce replaced by half its bytes
+        (PAPER.md:344).  step() waits for the outstanding buckets first.  Use
+        zero_grad() (which zeroes the arena in place) between steps."""
+        self.flat_grads()
+        ps = self.param_groups[0]["params"]
+        bucket_of = {}
+        for b, (_, _, tl) in enumerate(self.buckets):
+            for j in tl:
+                bucket_of[j] = b
+        self._rs_hooks = {"average": average, "bucket_of": bucket_of,
+                          "ready": [0] * len(self.buckets), "works": {},
+                          "handles": []}
+        for j, p in enumerate(ps):
+            self._rs_hooks["handles"].append(
+                p.register_post_accumulate_grad_hook(lambda _p, j=j: self._grad_ready(j)))
+
+    def _grad_ready(self, j: int):
+        h = self._rs_hooks
+        b = h["bucket_of"][j]
+        h["ready"][b] += 1
+        if h["ready"][b] == len(self.buckets[b][2]) and b not in h["works"]:
+            h["works"][b] = self._bucket_rs(b, h["average"], async_op=True)
+
+    def _finish_grad_reduce(self):
+        h = self._rs_hooks
+        for b in range(len(self.buckets)):
+            if b not in h["works"]:   # a bucket with unused parameters: reduce it now
+                h["works"][b] = self._bucket_rs(b, h["average"], async_op=True)
+        for w in h["works"].values():
+            if w is not None:
+                w.wait()
+        h["works"] = {}
+        h["ready"] = [0] * len(self.buckets)
+
+    def zero_grad(self, set_to_none: bool = True):
+        """With a gradient arena the views are kept and the arena is zeroed in
+        place (backward must accumulate into the arena)."""
+        if getattr(self, "_flat_grad", None) is not None:
+            self._flat_grad.zero_()
+            return
+        super().zero_grad(set_to_none=set_to_none)
+
+    def step(self, closure=None, loss=None):
+        if self._rs_hooks is not None:
+            if closure is not None:
+                with torch.enable_grad():
+                    loss = closure()
+                closure = None
+            self._finish_grad_reduce()
+        return super().step(closure=closure, loss=loss)
 
     def _slot(self, p, weight_slot=0) -> Slot:
         s = super()._slot(p, weight_slot)
@@ -259,15 +381,16 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
             dist.barrier(group=self.pg)
 
     def _gather(self):
-        S = self.slice_len
-        local = self.flat[self.rank * S:(self.rank + 1) * S]
-        if self._nccl():
-            # in place: input is this rank's slice of the output arena
-            dist.all_gather_into_tensor(self.flat, local, group=self.pg)
-        else:
-            chunks = [torch.empty(S, dtype=torch.float32) for _ in range(self.world)]
-            dist.all_gather(chunks, local.cpu(), group=self.pg)
-            self.flat.copy_(torch.cat(chunks).to(self.flat.device))
+        for base, S, _ in self.buckets:
+            seg = self.flat[base:base + self.world * S]
+            local = seg[self.rank * S:(self.rank + 1) * S]
+            if self._nccl():
+                # in place: input is this rank's portion of the output segment
+                dist.all_gather_into_tensor(seg, local, group=self.pg)
+            else:
+                chunks = [torch.empty(S, dtype=torch.float32) for _ in range(self.world)]
+                dist.all_gather(chunks, local.cpu(), group=self.pg)
+                seg.copy_(torch.cat(chunks).to(seg.device))
 
     def local_state_bytes(self) -> int:
         return sum(int(st["quad"].numel()) * 4 for st in self.state.values() if "quad" in st)

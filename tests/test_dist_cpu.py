@@ -236,3 +236,104 @@ def test_owner_layout_partitions_the_arena():
                 if w == rank:
                     seen[off:off + n] += 1
         assert seen.max() == 1 and seen.sum() == sum(sizes)
+
+
+def test_bucketed_layout_single_bucket_is_flat_layout():
+    from paper_2506_10315_b200.dist import bucketed_layout, flat_shard_ranges
+
+    sizes = [int(np.prod(s)) for s in SHAPES]
+    for world in (1, 2, 3, 4):
+        for rank in range(world):
+            r0, S, padded = flat_shard_ranges(sizes, world, rank)
+            r1, offsets, buckets, padded1 = bucketed_layout(sizes, world, rank)
+            assert r0 == r1 and padded == padded1 and buckets[0][1] == S
+            assert offsets == list(np.cumsum([0] + sizes[:-1]))
+
+
+def test_bucketed_layout_partitions_every_bucket():
+    from paper_2506_10315_b200.dist import bucketed_layout
+
+    sizes = [int(np.prod(s)) for s in SHAPES] + [1, 5000, 129]
+    order = list(reversed(range(len(sizes))))
+    for world in (1, 2, 4):
+        cover = {}
+        for rank in range(world):
+            ranges, offsets, buckets, padded = bucketed_layout(sizes, world, rank, 300, order)
+            assert sum(len(b[2]) for b in buckets) == len(sizes)
+            for base, S, tl in buckets:
+                assert S % 128 == 0
+                for j in tl:   # a tensor lies inside its bucket's segment
+                    assert base <= offsets[j] and offsets[j] + sizes[j] <= base + world * S
+            for j, (lo, hi) in enumerate(ranges):
+                for e in range(lo, hi):
+                    cover[(j, e)] = cover.get((j, e), 0) + 1
+        assert len(cover) == sum(sizes) and max(cover.values()) == 1
+
+
+def _overlap_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_10315_b200.dist import ShardedLearnedOptimizer
+
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(torch.nn.Linear(16, 32), torch.nn.ReLU(),
+                                    torch.nn.Linear(32, 8))
+        opt = ShardedLearnedOptimizer(model.parameters(), bucket_elems=200)
+        opt.overlap_grad_reduce(average=True)
+        g = torch.Generator().manual_seed(10 + rank)
+        x, y = torch.randn(4, 16, generator=g), torch.randn(4, 8, generator=g)
+        opt.zero_grad()
+        torch.nn.functional.mse_loss(model(x), y).backward()
+        launched = len(opt._rs_hooks["works"])   # buckets reduced during backward
+        opt._finish_grad_reduce()
+        ps = list(model.parameters())
+        out = [(opt.offsets[j], opt.state[p]["range"], p.grad.detach().reshape(-1).clone().numpy())
+               for j, p in enumerate(ps)]
+        q.put((rank, launched, len(opt.buckets), out))
+    except Exception:
+        import traceback
+        q.put((rank, -1, -1, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_reduce_scatter_overlapped_with_backward_gloo_world2():
+    """§8(f) rank 2: gradient buckets are reduce-scattered from inside
+    backward (post-accumulate-grad hooks); afterwards each rank holds the
+    mean gradient on its own element range of every tensor."""
+    import torch
+    import torch.multiprocessing as mp
+
+    torch.manual_seed(0)
+    model = torch.nn.Sequential(torch.nn.Linear(16, 32), torch.nn.ReLU(), torch.nn.Linear(32, 8))
+    grads = []
+    for r in range(2):
+        model.zero_grad()
+        g = torch.Generator().manual_seed(10 + r)
+        x, y = torch.randn(4, 16, generator=g), torch.randn(4, 8, generator=g)
+        torch.nn.functional.mse_loss(model(x), y).backward()
+        grads.append([p.grad.reshape(-1).clone().numpy() for p in model.parameters()])
+    mean = [(a + b) / np.float32(2) for a, b in zip(*grads)]
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=30)
+    for rank, launched, nb, out in res:
+        assert launched >= 0, out
+        assert nb > 1 and launched == nb
+        for (off, (lo, hi), g), m in zip(out, mean):
+            np.testing.assert_allclose(g[lo:hi], m[lo:hi], rtol=1e-6, atol=1e-9)

@@ -165,3 +165,91 @@ def test_exchange_off_updates_only_own_slice(gather):
             assert own.sum() == 0 or err.max() <= 1e-6
             err = np.abs(a[~own] - old[~own]) / (1 + np.abs(old[~own]))
             assert (~own).sum() == 0 or err.max() <= 1e-6
+
+
+def _overlap_step_worker(rank, world, port, q):
+    import sys
+    import traceback
+
+    sys.path.insert(0, ROOT)
+    try:
+        import torch
+        import torch.distributed as dist
+
+        from paper_2506_10315_b200.dist import ShardedLearnedOptimizer
+
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        model = _overlap_model()
+        opt = ShardedLearnedOptimizer(model.parameters(), mode="strict", weight_decay=0.01,
+                                      bucket_elems=1000)
+        opt.overlap_grad_reduce(average=True)
+        for step in range(2):
+            x, y = _overlap_batch(rank, step)
+            opt.zero_grad()
+            torch.nn.functional.mse_loss(model(x), y).backward()
+            opt.step()
+        torch.cuda.synchronize()
+        q.put((rank, [p.detach().cpu().numpy().copy() for p in model.parameters()],
+               len(opt.buckets)))
+        dist.destroy_process_group()
+    except Exception:
+        q.put((rank, traceback.format_exc(), 0))
+
+
+def _overlap_model():
+    import torch
+
+    torch.manual_seed(0)
+    return torch.nn.Sequential(torch.nn.Linear(64, 96), torch.nn.ReLU(),
+                               torch.nn.Linear(96, 33), torch.nn.ReLU(),
+                               torch.nn.Linear(33, 10)).cuda()
+
+
+def _overlap_batch(rank, step):
+    import torch
+
+    g = torch.Generator().manual_seed(1000 * step + rank)
+    return (torch.randn(8, 64, generator=g).cuda(), torch.randn(8, 10, generator=g).cuda())
+
+
+def test_backward_overlapped_reduce_scatter_step_bitwise():
+    """Data-parallel training step fed straight from backward (SURVEY.md
+    §8(f) rank 2): two ranks with different batches, bucketed gradient
+    reduce-scatter launched from post-accumulate-grad hooks, sharded strict
+    step -- bitwise equal to one process stepping with the mean gradient."""
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_2506_10315_b200 as P
+
+    model = _overlap_model()
+    opt = P.LearnedOptimizer(model.parameters(), mode="strict", weight_decay=0.01)
+    for step in range(2):
+        gs = []
+        for r in range(2):
+            model.zero_grad()
+            x, y = _overlap_batch(r, step)
+            torch.nn.functional.mse_loss(model(x), y).backward()
+            gs.append([p.grad.clone() for p in model.parameters()])
+        for p, a, b in zip(model.parameters(), *gs):
+            p.grad = (a + b) / 2
+        opt.step()
+    single = [p.detach().cpu().numpy() for p in model.parameters()]
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_step_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, out, nb in res:
+        assert not isinstance(out, str), out
+        assert nb > 1
+        for a, b in zip(out, single):
+            assert a.tobytes() == b.tobytes()
