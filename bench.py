@@ -490,17 +490,25 @@ def main():
         params, grads = make_model(args.workload, dev, seed=0)
         for p, g in zip(params, grads):
             p.grad = g
+        def timed_ms(o):
+            for _ in range(args.warmup):
+                o.step()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for _ in range(args.steps):
+                o.step()
+            a1.record()
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / args.steps
+
         aopt = torch.optim.AdamW(params, lr=1e-3, fused=True)
-        for _ in range(args.warmup):
-            aopt.step()
-        torch.cuda.synchronize()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record()
-        for _ in range(args.steps):
-            aopt.step()
-        a1.record()
-        torch.cuda.synchronize()
-        adam = {"torch_adamw_fused_ms_per_step": a0.elapsed_time(a1) / args.steps}
+        adam = {"torch_adamw_fused_ms_per_step": timed_ms(aopt)}
+        del aopt
+        # the hand-designed optimizer whose factored second moments small_fc_lopt's
+        # features build on (torch's foreach Adafactor)
+        aopt = torch.optim.Adafactor(params, lr=1e-2, foreach=True)
+        adam["torch_adafactor_foreach_ms_per_step"] = timed_ms(aopt)
         del aopt, params, grads
 
     cpu = None
@@ -512,6 +520,13 @@ def main():
                          f"oracle/ (bitwise restatement of the reference, 64-lane blocked MLP "
                          f"like engine.py:441-480, OpenMP over tensors), median of 3 steps",
                "ms_per_step_sample": r["step_s"] * 1e3}
+        # the shipped reference is single-threaded (numba,
+        # no parallel=True); the same port on one core, largest tensors first
+        r1 = run_cpu_oracle(args.workload, args.feature_set, 3_000_000, 1, 0, threads=1)
+        cpu["single_core"] = {"value": r1["params"] / r1["step_s"] / 1e9, "unit": "Gparams/s",
+                              "cores": 1, "sample": f"{r1['tensors']} {args.workload} tensors "
+                                                    f"(largest-first subset up to 3 M params) / "
+                                                    f"{r1['params']} params, one step"}
 
     if rank == 0:
         line = {
