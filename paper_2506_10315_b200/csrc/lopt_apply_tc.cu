@@ -334,7 +334,8 @@ __device__ __forceinline__ float max_nan_abs(float m, float x) {
 // Timing trace (LOPT_APPLY_DEBUG & 32): CTA 0 records clock64 at the pipeline
 // hand-offs of its first kTraceTiles tiles.
 constexpr int kTraceTiles = 64;
-__device__ long long g_trace[kTraceTiles][8];
+constexpr int kTraceEvents = 12;
+__device__ long long g_trace[kTraceTiles][kTraceEvents];
 __device__ __forceinline__ void trace(const DevicePlan &P, int32_t i, int ev) {
 #ifdef LOPT_TRACE
   if ((P.dbg & 32) && blockIdx.x == 0 && i < kTraceTiles && (threadIdx.x & 31) == 0)
@@ -605,6 +606,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       bv[14] = xl & 0xFFFFu;
       bv[15] = 0u;
       // TMEM slot is free once C has read the tile kSlots before
+      if (warp == 0) trace(P, i, 8);
       if (sc.wrapped) WAIT(&S.slot_free[sc.i], sc.phase ^ 1u, 6);
       tc::fence_after_sync();
       const uint32_t ta = tbase + lane_addr + 64 * sc.i;
@@ -625,6 +627,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     for (int32_t i = r0; i < nt; i += kStep) {
       // B touches neither the data ring nor the operand image (the layer-1
       // scale 2^-s2 is folded into W1): it waits for the accumulator only
+      if (warp == kWarpB) trace(P, i, 10);
       WAIT(&S.acc1_full[sc.i], sc.phase, 7);
       tc::fence_after_sync();
       if (warp == kWarpB) trace(P, i, 4);
@@ -678,6 +681,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       float *tp = mt.theta + row;
       const float w = (mt.flags & kFlagSlow) ? (valid ? *tp : 0.0f) : st.th[row];
       const PrepImage &ip = S.img[mt.img];
+      if (warp == kWarpC) trace(P, i, 9);
       WAIT(&S.acc2_full[sc.i], sc.phase, 8);
       tc::fence_after_sync();
       if (warp == kWarpC) trace(P, i, 6);
@@ -765,7 +769,7 @@ void launch_tc_apply(const DevicePlan &P0, cudaStream_t s) {
 }  // namespace lopt
 
 extern "C" int lopt_debug_apply_trace(long long *host, int32_t n) {
-  if (!host || n < 0 || n > lopt::kTraceTiles * 8) return LOPT_ERR_INVALID;
+  if (!host || n < 0 || n > lopt::kTraceTiles * lopt::kTraceEvents) return LOPT_ERR_INVALID;
   return cudaMemcpyFromSymbol(host, lopt::g_trace, sizeof(long long) * n) == cudaSuccess
              ? LOPT_OK
              : LOPT_ERR_CUDA;

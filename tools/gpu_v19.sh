@@ -1,0 +1,3 @@
+timeout 600 python -m pytest tests/test_gpu_fast.py tests/test_gpu_velo.py tests/test_gpu_fullsize.py -x -q 2>&1 | tail -2
+for k in 1 2; do timeout 300 python bench.py --no-cpu --no-e2e --no-velo 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['roofline'].get('phase_ms'))"; done
+bash tools/gpu_trace.sh $1

@@ -26,13 +26,18 @@ for _ in range(3):
     opt.step()
 torch.cuda.synchronize()
 L = _lib.lib()
-buf = (ctypes.c_longlong * (64 * 8))()
+buf = (ctypes.c_longlong * (64 * 12))()
 L.lopt_debug_apply_trace.argtypes = [ctypes.c_void_p, ctypes.c_int32]
-assert L.lopt_debug_apply_trace(ctypes.addressof(buf), 64 * 8) == 0
-t = np.array(buf[:], dtype=np.int64).reshape(64, 8)
-ev = t[0::2]          # the first warp of each role's warpgroup 0 records: even tiles
+assert L.lopt_debug_apply_trace(ctypes.addressof(buf), 64 * 12) == 0
+t = np.array(buf[:], dtype=np.int64).reshape(64, 12)
+# the first warp of each role's warpgroup 0 records: even tiles; columns in
+# pipeline order: prod, A data ready, A features done (before the TMEM slot
+# wait), A operands stored, MMA1, B loop top, B acc1 ready, MMA2, C before
+# acc2 wait, C acc2 ready, C done
+ev = t[0::2][:, [0, 1, 8, 2, 3, 10, 4, 5, 9, 6, 7]]
 ev = ev - ev[0, 0]
-names = ["prod", "A_in", "A_out", "mma1", "B_in", "mma2", "C_in", "C_end"]
+names = ["prod", "A_in", "A_feat", "A_out", "mma1", "B_top", "B_in", "mma2", "C_top", "C_in",
+         "C_end"]
 print("tile " + " ".join(f"{n:>8s}" for n in names))
 for k in range(ev.shape[0]):
     print(f"{2 * k:4d} " + " ".join(f"{v:8d}" for v in ev[k]))
