@@ -40,7 +40,8 @@
 namespace lopt {
 
 constexpr int kRing = 16;      // smem tile slots (prefetch + in flight)
-constexpr int kSlots = 7;      // TMEM tile slots
+constexpr int kSlots = 6;      // TMEM tile slots
+constexpr uint32_t kSlotCols = 80;   // per slot: 32 operand columns + 48 accumulator columns
 constexpr int kImgs = 4;       // smem operand images (tensor switches in flight)
 // warpgroups per role (tile i goes to warpgroup i % kWGs of the role) and
 // producer warps (tile i staged by producer i % kProducers)
@@ -51,7 +52,7 @@ constexpr int kWarpProducer = kWarpC + 4 * kWGsC;
 constexpr int kWarpMma1 = kWarpProducer + kProducers, kWarpMma2 = kWarpMma1 + 1;
 static_assert(kWGsA < kSlots && kWGsC < kSlots && kProducers < kRing, "cursor strides");
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kOneCol = 64 * kSlots;   // shared constant slice
+constexpr uint32_t kOneCol = kSlotCols * kSlots;   // shared constant slice
 static_assert(kOneCol + 8 <= kTmemCols, "TMEM budget");
 
 // kFlagTail: one of the last kWGsC tiles of its tensor -- the C warps publish
@@ -303,7 +304,7 @@ __device__ __forceinline__ void issue_layer1(uint64_t dimg, uint32_t op, uint32_
 
 __device__ __forceinline__ void issue_layer2(uint64_t dimg, uint32_t op, uint32_t acc,
                                              uint32_t one, uint64_t *bar) {
-  constexpr uint32_t idesc = tc::idesc_f16_f32(128, 32);
+  constexpr uint32_t idesc = tc::idesc_f16_f32(128, kN2);
   const uint64_t h0 = dimg + slice_off(offsetof(PrepImage, b2[0]));
   const uint64_t h1 = dimg + slice_off(offsetof(PrepImage, b2[1]));
   const uint64_t l0 = dimg + slice_off(offsetof(PrepImage, b2[2]));
@@ -502,7 +503,8 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     // --------------------------------------------------------------- MMA warps
     const bool l1 = warp == kWarpMma1;
     const uint32_t one = tbase + kOneCol;
-    const uint64_t dimg0 = tc::smem_desc_kmajor(tc::smem_u32(&S.img[0]), 512, 128);
+    // layer-1 slices are N = 32 rows (LBO 512 B), layer-2 slices N = 48 (LBO 768 B)
+    const uint64_t dimg0 = tc::smem_desc_kmajor(tc::smem_u32(&S.img[0]), l1 ? 512 : kN2 * 16, 128);
     Cursor<kRing> rc;
     Cursor<kSlots> sc;
     for (int32_t i = 0; i < nt; i++) {
@@ -511,7 +513,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       trace(P, i, l1 ? 3 : 5);
       const uint64_t dimg =
           dimg0 + (uint64_t)((uint32_t)S.stage[rc.i].meta.img * (uint32_t)(sizeof(PrepImage) >> 4));
-      const uint32_t op = tbase + 64 * sc.i, acc = op + 32;
+      const uint32_t op = tbase + kSlotCols * sc.i, acc = op + 32;
       if (tc::elect_one()) {
         if (l1) issue_layer1(dimg, op, acc, &S.acc1_full[sc.i]);
         else issue_layer2(dimg, op, acc, one, &S.acc2_full[sc.i]);
@@ -609,7 +611,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       if (warp == 0) trace(P, i, 8);
       if (sc.wrapped) WAIT(&S.slot_free[sc.i], sc.phase ^ 1u, 6);
       tc::fence_after_sync();
-      const uint32_t ta = tbase + lane_addr + 64 * sc.i;
+      const uint32_t ta = tbase + lane_addr + kSlotCols * sc.i;
       tc::tmem_st16(ta, ev);
       tc::tmem_st16(ta + 16, bv);
       tc::tmem_st_wait();
@@ -631,7 +633,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       WAIT(&S.acc1_full[sc.i], sc.phase, 7);
       tc::fence_after_sync();
       if (warp == kWarpB) trace(P, i, 4);
-      const uint32_t ta = tbase + lane_addr + 64 * sc.i;
+      const uint32_t ta = tbase + lane_addr + kSlotCols * sc.i;
 #pragma unroll
       for (int half = 0; half < 2; half++) {
         uint32_t h[16];
@@ -685,22 +687,24 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       WAIT(&S.acc2_full[sc.i], sc.phase, 8);
       tc::fence_after_sync();
       if (warp == kWarpC) trace(P, i, 6);
-      uint32_t h2[32];
-      tc::tmem_ld32(tbase + lane_addr + 64 * sc.i + 32, h2);
+      uint32_t h2[32], lin[2];
+      tc::tmem_ld32(tbase + lane_addr + kSlotCols * sc.i + 32, h2);
+      tc::tmem_ld2(tbase + lane_addr + kSlotCols * sc.i + 64, lin);
       tc::tmem_ld_wait();
       tc::fence_before_sync();
       warp_arrive(&S.slot_free[sc.i]);
-      // layer 3 in f32: four independent FFMA2 chains
-      float2 d0 = make_float2(ip.b3[0], 0.0f), d1 = make_float2(0.0f, 0.0f);
-      float2 m0 = make_float2(ip.b3[1], 0.0f), m1 = make_float2(0.0f, 0.0f);
-      const float4 *w3 = reinterpret_cast<const float4 *>(ip.w3i);
+      // layer 3 in f32: b3 + linear half (from the MMA) + sum (w3/2)|h2|,
+      // four independent FFMA2 chains, |x| as an operand modifier (no ReLU pass)
+      float2 d0 = make_float2(ip.b3[0] + __uint_as_float(lin[0]), 0.0f), d1 = make_float2(0.0f, 0.0f);
+      float2 m0 = make_float2(ip.b3[1] + __uint_as_float(lin[1]), 0.0f), m1 = make_float2(0.0f, 0.0f);
+      const float4 *w3 = reinterpret_cast<const float4 *>(ip.w3h);
 #pragma unroll
       for (int q = 0; q < 16; q += 2) {
         const float4 wa = w3[q], wb = w3[q + 1];
-        const float2 ha = make_float2(fmaxf(__uint_as_float(h2[2 * q]), 0.0f),
-                                      fmaxf(__uint_as_float(h2[2 * q + 1]), 0.0f));
-        const float2 hb = make_float2(fmaxf(__uint_as_float(h2[2 * q + 2]), 0.0f),
-                                      fmaxf(__uint_as_float(h2[2 * q + 3]), 0.0f));
+        const float2 ha = make_float2(fabsf(__uint_as_float(h2[2 * q])),
+                                      fabsf(__uint_as_float(h2[2 * q + 1])));
+        const float2 hb = make_float2(fabsf(__uint_as_float(h2[2 * q + 2])),
+                                      fabsf(__uint_as_float(h2[2 * q + 3])));
         d0 = ffma2(ha, make_float2(wa.x, wa.y), d0);
         m0 = ffma2(ha, make_float2(wa.z, wa.w), m0);
         d1 = ffma2(hb, make_float2(wb.x, wb.y), d1);

@@ -108,24 +108,42 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
     img->b1[2 * s][bslot(o, q)] = hi;
     img->b1[2 * s + 1][bslot(o, q)] = lo;
   }
-  // layer 2: W2 hi/lo by K halves, then the bias slice (k = 0: hi, k = 1: lo)
+  // layer 2: [W2 | v] hi/lo by K halves, then the bias slice (k = 0: hi, k = 1: lo).
+  // Rows 32/33 carry the linear half of layer 3 (see PrepImage): v_out[k] =
+  // 1/2 * 2^s2 * sum_o w3[out,o] W2[o,k] (its input is relu(h1) * 2^-s2) and the
+  // bias 1/2 * sum_o w3[out,o] b2[o]; summed in f64, rounded once.
   const float sd = s2s[0], su = s2s[1];
-  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
-    const int o = i >> 5, k = i & 31;
-    uint16_t hi, lo;
-    split1(w2[o * 32 + k], hi, lo);
-    img->b2[k >> 4][bslot(o, k & 15)] = hi;
-    img->b2[2 + (k >> 4)][bslot(o, k & 15)] = lo;
+  __shared__ float vrow[2][32], vbias[2];
+  if (threadIdx.x < 64) {
+    const int out = threadIdx.x >> 5, k = threadIdx.x & 31;
+    double acc = 0.0;
+    for (int o = 0; o < 32; o++) acc += (double)w3[out * 32 + o] * (double)w2[o * 32 + k];
+    vrow[out][k] = (float)(0.5 * (double)su * acc);
+  } else if (threadIdx.x < 66) {
+    const int out = threadIdx.x - 64;
+    double acc = 0.0;
+    for (int o = 0; o < 32; o++) acc += (double)w3[out * 32 + o] * (double)b2[o];
+    vbias[out] = (float)(0.5 * acc);
   }
-  for (int i = threadIdx.x; i < 32 * 16; i += blockDim.x) {
-    const int o = i >> 4, k = i & 15;
+  __syncthreads();
+  for (int i = threadIdx.x; i < kN2 * 32; i += blockDim.x) {
+    const int o = i >> 5, k = i & 31;
+    const float v = o < 32 ? w2[o * 32 + k] : (o < 34 ? vrow[o - 32][k] : 0.0f);
     uint16_t hi, lo;
-    split1(b2[o] * sd, hi, lo);
-    img->b2[4][bslot(o, k)] = k == 0 ? hi : (k == 1 ? lo : (uint16_t)0);
+    split1(v, hi, lo);
+    img->b2[k >> 4][bslot(o, k & 15, kN2)] = hi;
+    img->b2[2 + (k >> 4)][bslot(o, k & 15, kN2)] = lo;
+  }
+  for (int i = threadIdx.x; i < kN2 * 16; i += blockDim.x) {
+    const int o = i >> 4, k = i & 15;
+    const float b = o < 32 ? b2[o] * sd : (o < 34 ? vbias[o - 32] : 0.0f);
+    uint16_t hi, lo;
+    split1(b, hi, lo);
+    img->b2[4][bslot(o, k, kN2)] = k == 0 ? hi : (k == 1 ? lo : (uint16_t)0);
   }
   if (threadIdx.x < 64) {
     const int o = threadIdx.x & 31, out = threadIdx.x >> 5;
-    img->w3i[o >> 1][2 * out + (o & 1)] = w3[out * 32 + o] * su;
+    img->w3h[o >> 1][2 * out + (o & 1)] = w3[out * 32 + o] * su * 0.5f;
   }
   if (threadIdx.x < 2) img->b3[threadIdx.x] = b3[threadIdx.x];
   if (threadIdx.x < 3) img->sqmr[threadIdx.x] = sqrtf(P.tscal[j].mr[threadIdx.x]);

@@ -12,8 +12,9 @@ namespace lopt {
 
 constexpr int kTile = 128;
 
-// B slices are K=16 x N=32 fp16 in the canonical K-major no-swizzle layout:
-// byte (k>>3)*512 + (o>>3)*128 + (o&7)*16 + (k&7)*2.
+// B slices are K=16 x N fp16 in the canonical K-major no-swizzle layout:
+// byte (k>>3)*(N*16) + (o>>3)*128 + (o&7)*16 + (k&7)*2 (N = 32 for layer 1,
+// kN2 = 48 for layer 2; LBO = N*16 bytes, SBO = 128 bytes).
 //
 // Operands are fp16 two-term splits, x = x_hi + x_lo (relative residual
 // 2^-22), and every product is formed as x_hi*W_hi + x_lo*W_hi + x_hi*W_lo by
@@ -27,16 +28,24 @@ constexpr int kTile = 128;
 // layer-1 bias (so the MMA emits h1 * 2^-s2), the layer-2 bias is pre-scaled
 // by 2^-s2 and 2^s2 is folded into W3.
 //
+// Layer 3 without a ReLU pass: relu(h) = (h + |h|)/2, so
+//   dir = b3 + 1/2 sum_o w3[o] h2[o] + 1/2 sum_o w3[o] |h2[o]|.
+// The linear half is linear in relu(h1), so it rides on the layer-2 MMAs as
+// two extra output rows v = 1/2 W2^T w3 (bias 1/2 w3.b2): layer 2 runs with
+// N = 48 (rows 32, 33 = dir, mag; 34..47 zero) and the epilogue only forms
+// sum (w3/2) |h2| with FFMA2's |x| operand modifier.
+//
 // A operands (per 128-element tile, TMEM, 2 fp16 per 32-bit column):
 //   E_hi/E_lo  16 per-element features in elem_col order
 //   B_hi/B_lo  r5 r6 r7 rr5 rr6 rr7 | c5 c6 c7 rc5 rc6 rc7 | clip | 1 | 0 0
 //   H_hi/H_lo  32 hidden units of layer 1 (two K slices)
 //   ONE        {1, 1, 0, ...}: selects the layer-2 bias slice (b2_hi + b2_lo)
-// Layer 1 = 6 MMAs, layer 2 = 7 MMAs (M=128, N=32, K=16 each).
+// Layer 1 = 6 MMAs (M=128, N=32, K=16), layer 2 = 7 MMAs (M=128, N=48, K=16).
+constexpr int kN2 = 48;     // layer-2 MMA width: 32 hidden + {dir, mag} linear halves + pad
 struct __align__(128) PrepImage {
   uint16_t b1[4][512];      // W1 over E: hi, lo; W1 over B: hi, lo
-  uint16_t b2[5][512];      // W2_hi[K0-15], W2_hi[K16-31], W2_lo[K0-15], W2_lo[K16-31], bias
-  float w3i[16][4];         // {w3d[2q], w3d[2q+1], w3m[2q], w3m[2q+1]} * 2^s2
+  uint16_t b2[5][kN2 * 16]; // [W2|v]_hi[K0-15], _hi[K16-31], _lo[K0-15], _lo[K16-31], bias
+  float w3h[16][4];         // {w3d[2q], w3d[2q+1], w3m[2q], w3m[2q+1]} * 2^s2 / 2
   float escale[20];         // normalization scale of the per-element columns (+ clip), float4-read
   float b3[2];
   float sqmr[3];            // sqrt(mean r_i)
