@@ -687,28 +687,37 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       WAIT(&S.acc2_full[sc.i], sc.phase, 8);
       tc::fence_after_sync();
       if (warp == kWarpC) trace(P, i, 6);
-      uint32_t h2[32], lin[2];
-      tc::tmem_ld32(tbase + lane_addr + kSlotCols * sc.i + 32, h2);
-      tc::tmem_ld2(tbase + lane_addr + kSlotCols * sc.i + 64, lin);
-      tc::tmem_ld_wait();
-      tc::fence_before_sync();
-      warp_arrive(&S.slot_free[sc.i]);
       // layer 3 in f32: b3 + linear half (from the MMA) + sum (w3/2)|h2|,
-      // four independent FFMA2 chains, |x| as an operand modifier (no ReLU pass)
+      // four independent FFMA2 chains, |x| as an operand modifier (no ReLU
+      // pass); h2 is read in two 16-column halves to stay within 72 registers
+      const uint32_t tc2 = tbase + lane_addr + kSlotCols * sc.i + 32;
+      uint32_t h2[16], lin[2];
+      tc::tmem_ld16(tc2, h2);
+      tc::tmem_ld2(tc2 + 32, lin);
+      tc::tmem_ld_wait();
       float2 d0 = make_float2(ip.b3[0] + __uint_as_float(lin[0]), 0.0f), d1 = make_float2(0.0f, 0.0f);
       float2 m0 = make_float2(ip.b3[1] + __uint_as_float(lin[1]), 0.0f), m1 = make_float2(0.0f, 0.0f);
       const float4 *w3 = reinterpret_cast<const float4 *>(ip.w3h);
 #pragma unroll
-      for (int q = 0; q < 16; q += 2) {
-        const float4 wa = w3[q], wb = w3[q + 1];
-        const float2 ha = make_float2(fabsf(__uint_as_float(h2[2 * q])),
-                                      fabsf(__uint_as_float(h2[2 * q + 1])));
-        const float2 hb = make_float2(fabsf(__uint_as_float(h2[2 * q + 2])),
-                                      fabsf(__uint_as_float(h2[2 * q + 3])));
-        d0 = ffma2(ha, make_float2(wa.x, wa.y), d0);
-        m0 = ffma2(ha, make_float2(wa.z, wa.w), m0);
-        d1 = ffma2(hb, make_float2(wb.x, wb.y), d1);
-        m1 = ffma2(hb, make_float2(wb.z, wb.w), m1);
+      for (int half = 0; half < 2; half++) {
+        if (half == 1) {
+          tc::tmem_ld16(tc2 + 16, h2);
+          tc::tmem_ld_wait();
+          tc::fence_before_sync();
+          warp_arrive(&S.slot_free[sc.i]);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          const float4 wa = w3[8 * half + q], wb = w3[8 * half + q + 1];
+          const float2 ha = make_float2(fabsf(__uint_as_float(h2[2 * q])),
+                                        fabsf(__uint_as_float(h2[2 * q + 1])));
+          const float2 hb = make_float2(fabsf(__uint_as_float(h2[2 * q + 2])),
+                                        fabsf(__uint_as_float(h2[2 * q + 3])));
+          d0 = ffma2(ha, make_float2(wa.x, wa.y), d0);
+          m0 = ffma2(ha, make_float2(wa.z, wa.w), m0);
+          d1 = ffma2(hb, make_float2(wb.x, wb.y), d1);
+          m1 = ffma2(hb, make_float2(wb.z, wb.w), m1);
+        }
       }
       // the data slot (theta, meta) and the image are no longer needed
       warp_arrive(&S.data_free[rc.i]);
