@@ -55,6 +55,24 @@ def view_2d(shape) -> tuple:
     return (shape[0], int(np.prod(shape[1:])))
 
 
+def _flat_host_view(host, params):
+    """A 1-D float32 view over `host` when its tensors are consecutive,
+    contiguous pieces of one buffer in parameter order (then a tensor group is
+    one copy); None otherwise (per-tensor copies)."""
+    if not host or any(t.dtype != torch.float32 or not t.is_contiguous() for t in host):
+        return None
+    st = host[0].untyped_storage()
+    base, off = host[0].data_ptr(), 0
+    for t, p in zip(host, params):
+        if t.untyped_storage().data_ptr() != st.data_ptr() or t.data_ptr() != base + 4 * off:
+            return None
+        if t.numel() != p.numel():
+            return None
+        off += t.numel()
+    flat = torch.empty(0, dtype=torch.float32).set_(st, host[0].storage_offset(), (off,))
+    return flat
+
+
 class LearnedOptimizer(torch.optim.Optimizer):
     """Per-parameter MLP learned optimizer (small_fc_lopt / VeLO-MLP features).
 
@@ -136,10 +154,10 @@ class LearnedOptimizer(torch.optim.Optimizer):
             plan = StepPlan(slots, self.spec, weights, mode=self.mode)
             if getattr(self, "_peer_deltas", None):
                 plan.set_peers(self._peer_deltas)
-            self._plans[gi] = (key, plan, [s.grad.data_ptr() for s in slots])
+            self._plans[gi] = (key, plan, [(s.theta.data_ptr(), s.grad.data_ptr()) for s in slots])
         else:
             _, plan, ptrs = cached
-            now = [s.grad.data_ptr() for s in slots]
+            now = [(s.theta.data_ptr(), s.grad.data_ptr()) for s in slots]
             if now != ptrs:
                 plan.rebind(slots)
                 self._plans[gi] = (key, plan, now)
@@ -221,7 +239,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
 
     # -- host-buffer step (offload) ------------------------------------------
     @torch.no_grad()
-    def step_host(self, host_grads, host_params=None, *, chunks: int = 8):
+    def step_host(self, host_grads, host_params=None, *, chunks: int = 16):
         """One step with the gradients in (pinned) host memory and, if given,
         the updated parameters copied back into `host_params` -- the call a
         host-resident caller of the reference makes (opt_step with NumPy
@@ -245,11 +263,30 @@ class LearnedOptimizer(torch.optim.Optimizer):
             raise OptimError(f"got {len(host_params)} host parameter buffers for {len(params)}")
         key = (tuple(id(p) for p in params), chunks)
         hs = getattr(self, "_host_step", None)
+        if hs is not None and hs["key"] == key:
+            # the parameters and gradients must still be the arena views
+            pa, ga, offs = hs["parena"].data_ptr(), hs["garena"].data_ptr(), hs["offs"]
+            if any(p.data.data_ptr() != pa + 4 * offs[k] or p.grad is None
+                   or p.grad.data_ptr() != ga + 4 * offs[k] for k, p in enumerate(params)):
+                hs = None
         if hs is None or hs["key"] != key:
-            for p in params:
-                if p.grad is None:
-                    p.grad = torch.empty_like(p)
+            # device arenas: parameters and gradients re-homed as views of two
+            # flat buffers in parameter order, so a group of tensors moves
+            # across PCIe as one contiguous copy (per-tensor copies cost a few
+            # microseconds each on the copy engines; ViT-B/16 has 152 tensors)
             total = sum(p.numel() for p in params)
+            dev = params[0].device
+            parena = torch.empty(total, dtype=torch.float32, device=dev)
+            garena = torch.zeros(total, dtype=torch.float32, device=dev)
+            offs, off = [], 0
+            for p in params:
+                n = p.numel()
+                parena[off:off + n].copy_(p.data.reshape(-1))
+                p.data = parena[off:off + n].view(p.shape)
+                p.grad = garena[off:off + n].view(p.shape)
+                offs.append(off)
+                off += n
+            offs.append(off)
             groups, cur, acc = [], [], 0
             for k, p in enumerate(params):
                 cur.append(k)
@@ -260,8 +297,12 @@ class LearnedOptimizer(torch.optim.Optimizer):
             if cur:
                 groups.append(cur)
             hs = {"key": key, "groups": groups, "plans": [None] * len(groups),
-                  "h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream()}
+                  "h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream(),
+                  "parena": parena, "garena": garena, "offs": offs}
             self._host_step = hs
+        offs = hs["offs"]
+        hg_flat = _flat_host_view(host_grads, params)
+        hp_flat = _flat_host_view(host_params, params) if host_params is not None else None
         group = self.param_groups[0]
         lr = schedule_lr(self.schedule, self.T) if self.schedule is not None else group["lr"]
         wd, t = group["weight_decay"], self.T + 1
@@ -271,8 +312,12 @@ class LearnedOptimizer(torch.optim.Optimizer):
         h2d.wait_stream(comp)        # the previous step is done reading the grads
         with torch.cuda.stream(h2d):
             for ks in hs["groups"]:
-                for k in ks:
-                    params[k].grad.copy_(host_grads[k].view(params[k].shape), non_blocking=True)
+                if hg_flat is not None:
+                    o0, o1 = offs[ks[0]], offs[ks[-1] + 1]
+                    hs["garena"][o0:o1].copy_(hg_flat[o0:o1], non_blocking=True)
+                else:
+                    for k in ks:
+                        params[k].grad.copy_(host_grads[k].view(params[k].shape), non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d)
                 uploaded.append(ev)
@@ -298,9 +343,13 @@ class LearnedOptimizer(torch.optim.Optimizer):
                 done.record(comp)
                 d2h.wait_event(done)
                 with torch.cuda.stream(d2h):
-                    for k in ks:
-                        host_params[k].view(params[k].shape).copy_(params[k].detach(),
-                                                                    non_blocking=True)
+                    if hp_flat is not None:
+                        o0, o1 = offs[ks[0]], offs[ks[-1] + 1]
+                        hp_flat[o0:o1].copy_(hs["parena"][o0:o1], non_blocking=True)
+                    else:
+                        for k in ks:
+                            host_params[k].view(params[k].shape).copy_(params[k].detach(),
+                                                                        non_blocking=True)
         comp.wait_stream(d2h)
         self._pending = launched
         self._last = launched

@@ -172,10 +172,13 @@ def test_fast_zero_network_is_noop(P):
 
 
 @pytest.mark.parametrize("mode", ["strict", "fast"])
-def test_step_host_matches_device_step(P, mode):
+@pytest.mark.parametrize("flat_host", [False, True])
+def test_step_host_matches_device_step(P, mode, flat_host):
     """step_host (chunked H2D / step / D2H pipeline) gives the same parameters
     and state as step() on device-resident gradients -- bitwise, since both
-    run the same kernels on the same tensors."""
+    run the same kernels on the same tensors.  flat_host: the host tensors are
+    consecutive views of one pinned buffer, so each tensor group moves as one
+    copy; otherwise per-tensor copies."""
     import torch
 
     shapes = [(128, 784), (128,), (10, 128), (10,), (256, 256), (33, 70)]
@@ -187,12 +190,28 @@ def test_step_host_matches_device_step(P, mode):
     b = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
     oa = P.LearnedOptimizer(a, mode=mode, weight_decay=0.01)
     ob = P.LearnedOptimizer(b, mode=mode, weight_decay=0.01)
-    host_p = [torch.empty(s, dtype=torch.float32).pin_memory() for s in shapes]
+    sizes = [int(np.prod(s)) for s in shapes]
+    offs = np.cumsum([0] + sizes)
+
+    def host_views(buf):
+        return [buf[offs[k]:offs[k + 1]].view(s) for k, s in enumerate(shapes)]
+
+    if flat_host:
+        host_p = host_views(torch.empty(offs[-1], dtype=torch.float32).pin_memory())
+    else:
+        host_p = [torch.empty(s, dtype=torch.float32).pin_memory() for s in shapes]
     for gs in grads:
         for p, g in zip(a, gs):
             p.grad = torch.from_numpy(g).cuda()
         oa.step()
-        ob.step_host([torch.from_numpy(g).pin_memory() for g in gs], host_p, chunks=3)
+        if flat_host:
+            hg = host_views(torch.from_numpy(np.concatenate([g.reshape(-1) for g in gs])).pin_memory())
+        else:
+            hg = [torch.from_numpy(g).pin_memory() for g in gs]
+        ob.step_host(hg, host_p, chunks=3)
+    from paper_2506_10315_b200.optim import _flat_host_view
+
+    assert (_flat_host_view(host_p, b) is not None) == flat_host
     torch.cuda.synchronize()
     for p, q, h in zip(a, b, host_p):
         assert p.detach().cpu().numpy().tobytes() == q.detach().cpu().numpy().tobytes()

@@ -38,3 +38,14 @@ for ch in (4, 8, 16, 32):
     for _ in range(5): opt.step_host(hg, hp, chunks=ch)
     b.record(); torch.cuda.synchronize()
     print("chunks", ch, f"{a.elapsed_time(b)/5:.2f} ms")
+# host enqueue cost of one step_host call (the GPU may wait on the CPU)
+for ch in (8, 32):
+    opt._host_step = None
+    for _ in range(3): opt.step_host(hg, hp, chunks=ch)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5): opt.step_host(hg, hp, chunks=ch)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print("chunks", ch, f"enqueue {(t1 - t0) / 5 * 1e3:.2f} ms/step, wall {(t2 - t0) / 5 * 1e3:.2f} ms/step")
