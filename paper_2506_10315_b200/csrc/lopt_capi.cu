@@ -256,7 +256,7 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   take(p->r_sumsq, sizeof(double) * D * count);
   take(p->r_weights, sizeof(float) * (size_t)wstride * cfg->num_weight_sets);
   take(p->r_prep, fast ? prep_image_bytes() * count : 16);
-  take(p->r_bcsum, fast ? sizeof(double) * D * count : 16);
+  take(p->r_bcsum, sizeof(double) * D * count);   // closed-form broadcast sums (both modes)
   p->ws_bytes = align_up(off, 256);
   // device plan (pointers filled at bind time)
   DevicePlan &P = p->dp;
@@ -341,7 +341,7 @@ int lopt_bind_workspace(lopt_plan *p, void *dev_ptr, size_t bytes, void *stream)
   P.grad_flag = fsums + (p->factor_sums - 1);
   const bool fast = p->cfg.mode == LOPT_MODE_FAST;
   P.prep = fast ? (unsigned char *)(ws + p->r_prep.off) : nullptr;
-  P.bcsum = fast ? (double *)(ws + p->r_bcsum.off) : nullptr;
+  P.bcsum = (double *)(ws + p->r_bcsum.off);
   int st;
   if ((st = check_cuda(cudaMemsetAsync(ws + p->r_bcsum.off, 0, p->r_bcsum.bytes, s)))) return st;
   // descriptor uploads: pageable source, so the copies complete before return

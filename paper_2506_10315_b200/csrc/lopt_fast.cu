@@ -347,6 +347,12 @@ void launch_fast_stats(const DevicePlan &P, cudaStream_t s) {
   stats_reduce_fast_kernel<<<P.count, 256, 0, s>>>(P);
 }
 
+// strict mode: the same per-tensor reduction (item partials of the per-element
+// columns + closed-form broadcast and time columns, all f64)
+void launch_stats_reduce_closed(const DevicePlan &P, cudaStream_t s) {
+  stats_reduce_fast_kernel<<<P.count, 256, 0, s>>>(P);
+}
+
 void launch_tc_apply(const DevicePlan &P, cudaStream_t s);
 
 void launch_fast_apply(const DevicePlan &P, cudaStream_t s) {

@@ -9,6 +9,7 @@
 // (lopt_fast.cu) is the product path; this one is the yardstick.
 #include "lopt_common.cuh"
 #include "lopt_tc.cuh"
+#include "lopt_fast.cuh"
 
 namespace lopt {
 
@@ -71,21 +72,29 @@ __device__ __forceinline__ void unpack_elem(const RawElem &r, bool advanced, con
 }
 
 // Phase 1 (engine.py:619-654 fused_stats): per-element features, f64 sums of
-// squares, block reduction in a fixed order -> stat_part[item][k].
+// squares of the 16 (VeLO: 17) per-element columns -> stat_part[item][col]
+// (0 for the others).  The 12 row/column-broadcast columns and the 11 time
+// columns are per-row / per-column / per-tensor constants whose sums have
+// closed forms (count x value^2, factor_means_kernel and
+// stats_reduce_fast_kernel); any f64 summation order reproduces the f32
+// normalization scale, so only the per-element
+// columns need per-thread f64 accumulators -- 16 instead of 39 doubles,
+// which is what lets the kernel hold two elements' loads in flight.
 template <int KIND>
-__global__ void __launch_bounds__(kStrictThreads)
+__global__ void __launch_bounds__(kStrictThreads, 3)
 stats_strict_kernel(DevicePlan P) {
   constexpr int D = d_feat(KIND);
+  constexpr int NE = KIND == LOPT_VELO_MLP ? 17 : 16;
   const ChunkItem it = P.stat_items[blockIdx.x];
   const TensorDesc T = P.tensors[it.tensor];
   const TensorScalars ts = P.tscal[it.tensor];
   __shared__ float tf[kTimeFeatures];
-  __shared__ double red[kStrictThreads / 32][D];
+  __shared__ double red[kStrictThreads / 32][NE];
   if (threadIdx.x < kTimeFeatures) tf[threadIdx.x] = P.step->tf[threadIdx.x];
   __syncthreads();
-  double acc[D];
+  double acc[NE];
 #pragma unroll
-  for (int k = 0; k < D; k++) acc[k] = 0.0;
+  for (int k = 0; k < NE; k++) acc[k] = 0.0;
   auto accumulate = [&](const RawElem &r) {
     Elem x;
     float4 ns;
@@ -93,9 +102,9 @@ stats_strict_kernel(DevicePlan P) {
     unpack_elem(r, P.state_advanced, P.beta, x, ns, rowt, colt);
     strict_features<KIND>(x, rowt, colt, ts.mr, tf, f);
 #pragma unroll
-    for (int k = 0; k < D; k++) {
-      const double fv = (double)f[k];
-      acc[k] = __fma_rn(fv, fv, acc[k]);
+    for (int q = 0; q < NE; q++) {
+      const double fv = (double)f[q < 16 ? elem_col(KIND, q) : 28];
+      acc[q] = __fma_rn(fv, fv, acc[q]);
     }
   };
   for (int64_t e = it.e0 + threadIdx.x; e < it.e1; e += 2 * kStrictThreads) {
@@ -108,28 +117,21 @@ stats_strict_kernel(DevicePlan P) {
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int k = 0; k < D; k++) {
-    const double s = warp_sum(acc[k]);
-    if (lane == 0) red[warp][k] = s;
+  for (int q = 0; q < NE; q++) {
+    const double s = warp_sum(acc[q]);
+    if (lane == 0) red[warp][q] = s;
   }
   __syncthreads();
-  if (threadIdx.x < D) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kStrictThreads / 32; w++) s += red[w][threadIdx.x];
-    P.stat_part[(int64_t)blockIdx.x * D + threadIdx.x] = s;
-  }
-}
-
-// Per-tensor sums of the phase-1 item partials, in item order.
-__global__ void stats_reduce_kernel(DevicePlan P) {
-  const int j = blockIdx.x;
-  const TensorDesc T = P.tensors[j];
-  const int D = d_feat(P.kind);
-  for (int k = threadIdx.x; k < D; k += blockDim.x) {
-    double s = 0.0;
-    for (int i = 0; i < T.stat_items; i++) s += P.stat_part[(int64_t)(T.stat_item0 + i) * D + k];
-    T.sumsq[k] = s;
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    int q = -1;
+    for (int s2 = 0; s2 < 16; s2++)
+      if (elem_col(KIND, s2) == c) q = s2;
+    if (KIND == LOPT_VELO_MLP && c == 28) q = 16;
+    double v = 0.0;
+    if (q >= 0) {
+      for (int w = 0; w < kStrictThreads / 32; w++) v += red[w][q];
+    }
+    P.stat_part[(int64_t)blockIdx.x * D + c] = v;
   }
 }
 
@@ -336,8 +338,9 @@ void launch_strict_stats(const DevicePlan &P, cudaStream_t s) {
     stats_strict_kernel<LOPT_VELO_MLP><<<P.n_stat_items, kStrictThreads, 0, s>>>(P);
 }
 
+void launch_stats_reduce_closed(const DevicePlan &P, cudaStream_t s);
 void launch_stats_reduce(const DevicePlan &P, cudaStream_t s) {
-  stats_reduce_kernel<<<P.count, 64, 0, s>>>(P);
+  launch_stats_reduce_closed(P, s);
 }
 
 void launch_strict_apply(const DevicePlan &P, cudaStream_t s) {
