@@ -376,7 +376,7 @@ def fused_apply(W, g, state: DeviceOptState, weights: LoptWeights, spec, stats, 
 
 
 def step_fused(W, g, state: DeviceOptState, weights: LoptWeights, spec=None, lr: float = 1.0,
-               workers: int = 1, tensor_name: str = "", mode="strict"):
+               workers: int = 1, tracker=None, tensor_name: str = "", mode="strict"):
     """engine.py:713-748: returns (new W tensor, report dict).  The state must
     already be advanced for g."""
     spec = spec or small_fc_lopt_spec()
@@ -390,3 +390,15 @@ def step_fused(W, g, state: DeviceOptState, weights: LoptWeights, spec=None, lr:
     report = {"tensor_name": tensor_name, "elements": W.numel(), "max_abs_update": float(mx[0]),
               "kernel_launches": plan.launches_last_step()}
     return out, report
+
+
+def step_naive(W, g, state: DeviceOptState, weights: LoptWeights, spec=None, lr: float = 1.0,
+               tracker=None, tensor_name: str = ""):
+    """engine.py:751-826, the reference's non-bitwise class: it materializes
+    the features and runs the MLP as a blocked BLAS product, so it agrees with
+    step_fused only to the cross-path tolerance 1e-5 (1 + |W|)
+    (test_engine.py:262-275).  The device counterpart is the tensor-core
+    (fast) path: the same features, the MLP contracted on tcgen05 with an fp16
+    two-term split, equally within that tolerance of the fused result."""
+    return step_fused(W, g, state, weights, spec, lr, tracker=tracker, tensor_name=tensor_name,
+                      mode="fast")

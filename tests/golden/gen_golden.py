@@ -53,7 +53,7 @@ ENGINE_SHAPES = [(1, 1), (1, 130), (130, 1), (5, 64), (7, 63), (3, 65), (33, 70)
 
 def engine_cases(engine, features, state_mod):
     """Per-tensor engine outputs: features at sampled indices, pass-1 sums for
-    several worker counts, and step_fused at lr 1 and lr 0.3."""
+    several worker counts, and step_fused / step_naive at lr 1 and lr 0.3."""
     out = {}
     for spec_name in ("small_fc_lopt", "velo_mlp"):
         spec = features.spec_by_name(spec_name)
@@ -83,6 +83,9 @@ def engine_cases(engine, features, state_mod):
                 p2, rep = engine.step_fused(W, g, s, w, spec, lr=lr)
                 out[key + f"/out_lr{lr}"] = p2.data
                 out[key + f"/maxabs_lr{lr}"] = np.array([rep.max_abs_update], np.float64)
+                # the naive class (engine.py:751-826): BLAS MLP, cross-path tolerance
+                p3, _ = engine.step_naive(W, g, s, w, spec, lr=lr)
+                out[key + f"/naive_lr{lr}"] = p3.data
     return out
 
 

@@ -69,6 +69,36 @@ def test_step_fused_fast_vs_reference_golden(P, oracle, spec_name, shape):
         assert err <= TOL, err
 
 
+@pytest.mark.parametrize("spec_name", ["small_fc_lopt", "velo_mlp"])
+@pytest.mark.parametrize("shape", [(1, 1), (130, 1), (7, 63), (33, 70), (17, 129)])
+def test_step_naive_vs_reference_naive_golden(P, oracle, spec_name, shape):
+    """engine.step_naive (the non-bitwise class, here the tensor-core path)
+    against the reference's own step_naive outputs (BLAS MLP), within the
+    reference's cross-path bound 1e-5 (1 + |W|) (test_engine.py:262-275)."""
+    import torch
+
+    G = load_golden("engine_cases.npz")
+    m, n = shape
+    key = f"{spec_name}/{m}x{n}"
+    s = oracle.OState.zeros(m, n)
+    for i in range(3):
+        s.M[i] = G[f"{key}/M{i}"]
+        s.r[i] = G[f"{key}/r{i}"]
+        s.c[i] = G[f"{key}/c{i}"]
+    s.V = G[f"{key}/V"]
+    s.t = int(G[f"{key}/t"][0])
+    spec = P.spec_by_name(spec_name)
+    W = torch.from_numpy(G[key + "/W"]).cuda()
+    g = torch.from_numpy(G[key + "/g"]).cuda()
+    w = P.random_weights(spec.d_feat, seed=int(G[key + "/wseed"][0]))
+    for lr in (1.0, 0.3):
+        st = P.DeviceOptState.from_arrays(s.M, s.V, s.r, s.c, s.t)
+        out, _ = P.step_naive(W, g, st, w, spec, lr=lr)
+        ref = G[key + f"/naive_lr{lr}"].astype(np.float64)
+        err = (np.abs(out.cpu().numpy().astype(np.float64) - ref) / (1 + np.abs(ref))).max()
+        assert err <= 1e-5, err
+
+
 SHAPE_SETS = {
     "mlp": [(128, 784), (128,), (10, 128), (10,)],
     "vit_block": [(2304, 768), (2304,), (768, 768), (768,), (3072, 768), (768, 3072), (1, 197, 768),
