@@ -253,6 +253,12 @@ class LearnedOptimizer(torch.optim.Optimizer):
         non-finite gradient aborts its group (groups already stepped stay
         committed -- documented difference to the all-or-nothing opt_step).
         Returns after enqueueing; host_params are valid after a device sync.
+
+        On the first call (and whenever a parameter was moved since) the
+        parameters and their gradients are re-homed into two device arenas:
+        `p.data` / `p.grad` become views of flat buffers in parameter order.
+        When `host_grads` / `host_params` are consecutive views of one pinned
+        buffer in the same order, every group crosses PCIe as one copy.
         """
         params = [p for g in self.param_groups for p in g["params"]]
         if len(self.param_groups) != 1:
