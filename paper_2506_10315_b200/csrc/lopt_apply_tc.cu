@@ -18,11 +18,11 @@
 //   WG_A (128 thr) features -> E/B operands in TMEM slot   --op_ready-->
 //   MMA warp L1    6 x tcgen05.mma -> acc                  --acc1_full-->
 //   WG_B (128 thr) ReLU + fp16 split of h1 -> H operand    --h_ready-->
-//   MMA warp L2    7 x tcgen05.mma -> acc                  --acc2_full-->
-//   WG_C (128 thr) ReLU, layer 3, exp, update, store theta --slot_free/data_free-->
+//   MMA warp L2    7 x tcgen05.mma (N = 48) -> acc         --acc2_full-->
+//   WG_C (128 thr) layer 3 (|h2| FFMA2s + MMA linear half), exp, update, store theta --slot_free/data_free-->
 //
 // Thread i of each warpgroup owns TMEM lane i = lane i of every tile.  TMEM
-// holds kSlots tiles in flight (64 columns each: operands, accumulator), so
+// holds kSlots tiles in flight (kSlotCols = 80 columns each: 32 operand, 48 accumulator), so
 // MMA latency is hidden by the other tiles' CUDA-core work instead of being
 // waited out.  All hand-offs are mbarriers; MMAs are issued by one elected
 // lane of a converged warp (descriptors in uniform registers, back-to-back
