@@ -290,3 +290,42 @@ def test_fused_peer_copies_single_gpu(P):
     assert torch.equal(arena, ref_arena)
     for q in peers:
         assert torch.equal(q, arena)
+
+
+@pytest.mark.parametrize("b2_shift", [-3.0, 3.0])
+def test_fast_layer3_split_accuracy_with_skewed_hidden_layer(P, oracle, b2_shift):
+    """The fast epilogue forms relu(h2).w3 as 1/2 w3.h2 (on the tensor cores,
+    layer-2 extra rows) + 1/2 w3.|h2| (FFMA2).  A layer-2 bias pushed far
+    negative makes most h2 < 0, so the two halves nearly cancel; pushed
+    positive, relu is the identity.  Both stay inside the reference's
+    cross-path bound 1e-5 (1 + |theta|)."""
+    import torch
+
+    shapes = [(128, 784), (128,), (10, 128), (10,), (33, 70)]
+    rng = np.random.default_rng(21)
+    init = [np.asarray(rng.standard_normal(s) * 0.02, dtype=F32) for s in shapes]
+    ow = oracle.random_weights(39, seed=3)
+    layers = [(w.copy(), b.copy()) for w, b in ow.layers]
+    w2, b2 = layers[1]
+    layers[1] = (w2, (b2 + np.float32(b2_shift)).astype(F32))
+    w3, b3 = layers[2]
+    layers[2] = ((w3 * np.float32(4.0)).astype(F32), b3)
+    ow.layers = layers
+    pw = P.LoptWeights(layers=[(w.copy(), b.copy()) for w, b in layers])
+    params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    opt = P.LearnedOptimizer(params, mode="fast", weights=pw)
+    o_params = [x.reshape(P.view_2d(x.shape)).copy() for x in init]
+    o_states = [oracle.OState.zeros(*p.shape) for p in o_params]
+    worst = 0.0
+    for step in range(2):
+        grads = [(rng.standard_normal(p.shape) * 1e-3).astype(F32) for p in o_params]
+        for p, q in zip(params, o_params):
+            p.data.copy_(torch.from_numpy(q.reshape(p.shape)).cuda())
+        for p, g in zip(params, grads):
+            p.grad = torch.from_numpy(g.reshape(p.shape)).cuda()
+        opt.step()
+        oracle.opt_step(o_params, o_states, grads, ow, oracle.SMALL_FC_LOPT, 1.0, threads=8)
+        for p, q in zip(params, o_params):
+            worst = max(worst, _close(p.detach().cpu().numpy(), q))
+    print(f"b2 shift {b2_shift}: max err/(1+|theta|) {worst:.3e}")
+    assert worst <= TOL, worst
