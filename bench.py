@@ -258,9 +258,9 @@ def time_device(opt, params, grads, steps, warmup, world):
 
 
 # tensor groups of the host-buffer step: finer groups shorten the pipeline's
-# fill (first upload) and drain (last download); 16 measured best (8.3 ms vs 8.5
-# with 8 and 9.9 with 32, where per-group host launch overhead shows)
-E2E_CHUNKS = int(os.environ.get("LOPT_E2E_CHUNKS", "16"))
+# fill (first upload) and drain (last download); with double-buffered gradient
+# arenas 8 and 16 measure alike (8.0 ms), 32 is host-launch bound (9.8 ms)
+E2E_CHUNKS = int(os.environ.get("LOPT_E2E_CHUNKS", "8"))
 
 
 def time_e2e(opt, params, grads, steps, warmup, world):

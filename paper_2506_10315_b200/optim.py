@@ -239,7 +239,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
 
     # -- host-buffer step (offload) ------------------------------------------
     @torch.no_grad()
-    def step_host(self, host_grads, host_params=None, *, chunks: int = 16):
+    def step_host(self, host_grads, host_params=None, *, chunks: int = 8):
         """One step with the gradients in (pinned) host memory and, if given,
         the updated parameters copied back into `host_params` -- the call a
         host-resident caller of the reference makes (opt_step with NumPy
@@ -258,7 +258,9 @@ class LearnedOptimizer(torch.optim.Optimizer):
         parameters and their gradients are re-homed into two device arenas:
         `p.data` / `p.grad` become views of flat buffers in parameter order.
         When `host_grads` / `host_params` are consecutive views of one pinned
-        buffer in the same order, every group crosses PCIe as one copy.
+        buffer in the same order, every group crosses PCIe as one copy.  Two
+        gradient arenas alternate between calls, so a call's uploads overlap
+        the previous call's last groups; `p.grad` views the first arena.
         """
         params = [p for g in self.param_groups for p in g["params"]]
         if len(self.param_groups) != 1:
@@ -271,7 +273,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
         hs = getattr(self, "_host_step", None)
         if hs is not None and hs["key"] == key:
             # the parameters and gradients must still be the arena views
-            pa, ga, offs = hs["parena"].data_ptr(), hs["garena"].data_ptr(), hs["offs"]
+            pa, ga, offs = hs["parena"].data_ptr(), hs["garena"][0].data_ptr(), hs["offs"]
             if any(p.data.data_ptr() != pa + 4 * offs[k] or p.grad is None
                    or p.grad.data_ptr() != ga + 4 * offs[k] for k, p in enumerate(params)):
                 hs = None
@@ -283,13 +285,15 @@ class LearnedOptimizer(torch.optim.Optimizer):
             total = sum(p.numel() for p in params)
             dev = params[0].device
             parena = torch.empty(total, dtype=torch.float32, device=dev)
-            garena = torch.zeros(total, dtype=torch.float32, device=dev)
+            # two gradient arenas, used alternately: the next call's uploads
+            # need not wait for this call's last group to finish computing
+            garena = [torch.zeros(total, dtype=torch.float32, device=dev) for _ in range(2)]
             offs, off = [], 0
             for p in params:
                 n = p.numel()
                 parena[off:off + n].copy_(p.data.reshape(-1))
                 p.data = parena[off:off + n].view(p.shape)
-                p.grad = garena[off:off + n].view(p.shape)
+                p.grad = garena[0][off:off + n].view(p.shape)
                 offs.append(off)
                 off += n
             offs.append(off)
@@ -302,7 +306,9 @@ class LearnedOptimizer(torch.optim.Optimizer):
                     cur = []
             if cur:
                 groups.append(cur)
-            hs = {"key": key, "groups": groups, "plans": [None] * len(groups),
+            hs = {"key": key, "groups": groups,
+                  "plans": [[None] * len(groups), [None] * len(groups)],
+                  "ptrs": [{}, {}], "read_done": [None, None], "parity": 0,
                   "h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream(),
                   "parena": parena, "garena": garena, "offs": offs}
             self._host_step = hs
@@ -315,15 +321,23 @@ class LearnedOptimizer(torch.optim.Optimizer):
         comp = torch.cuda.current_stream()
         h2d, d2h = hs["h2d"], hs["d2h"]
         uploaded = []
-        h2d.wait_stream(comp)        # the previous step is done reading the grads
+        b = hs["parity"]
+        hs["parity"] ^= 1
+        garena = hs["garena"][b]
+        # this buffer was last read by the step before the previous one
+        if hs["read_done"][b] is not None:
+            h2d.wait_event(hs["read_done"][b])
+        else:
+            h2d.wait_stream(comp)
         with torch.cuda.stream(h2d):
             for ks in hs["groups"]:
                 if hg_flat is not None:
                     o0, o1 = offs[ks[0]], offs[ks[-1] + 1]
-                    hs["garena"][o0:o1].copy_(hg_flat[o0:o1], non_blocking=True)
+                    garena[o0:o1].copy_(hg_flat[o0:o1], non_blocking=True)
                 else:
                     for k in ks:
-                        params[k].grad.copy_(host_grads[k].view(params[k].shape), non_blocking=True)
+                        garena[offs[k]:offs[k + 1]].copy_(host_grads[k].reshape(-1),
+                                                          non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(h2d)
                 uploaded.append(ev)
@@ -332,16 +346,18 @@ class LearnedOptimizer(torch.optim.Optimizer):
         for gi, ks in enumerate(hs["groups"]):
             comp.wait_event(uploaded[gi])
             ps = [params[k] for k in ks]
-            plan = hs["plans"][gi]
+            plan = hs["plans"][b][gi]
             slots = [self._slot(p) for p in ps]
-            ptrs = [s.grad.data_ptr() for s in slots]
+            for k, sl in zip(ks, slots):
+                sl.grad = garena[offs[k]:offs[k + 1]]
+            ptrs = [(sl.theta.data_ptr(), sl.grad.data_ptr()) for sl in slots]
             if plan is None:
                 plan = StepPlan(slots, self.spec, self.lopt_weights, mode=self.mode)
-                hs["plans"][gi] = plan
-                hs.setdefault("ptrs", {})[gi] = ptrs
-            elif hs["ptrs"][gi] != ptrs:
+                hs["plans"][b][gi] = plan
+                hs["ptrs"][b][gi] = ptrs
+            elif hs["ptrs"][b][gi] != ptrs:
                 plan.rebind(slots)
-                hs["ptrs"][gi] = ptrs
+                hs["ptrs"][b][gi] = ptrs
             plan.step(lr, wd, t)
             launched.append((plan, ps))
             if host_params is not None:
@@ -356,7 +372,10 @@ class LearnedOptimizer(torch.optim.Optimizer):
                         for k in ks:
                             host_params[k].view(params[k].shape).copy_(params[k].detach(),
                                                                         non_blocking=True)
-        comp.wait_stream(d2h)
+        ev = torch.cuda.Event()
+        ev.record(comp)              # the last group has read gradient buffer b
+        hs["read_done"][b] = ev
+        comp.wait_stream(d2h)        # the next step's applies write what these copies read
         self._pending = launched
         self._last = launched
         if self.check_errors:
