@@ -115,6 +115,112 @@ __device__ void factor_tile(const DevicePlan &P, const FactorItem &it, const Ten
   if (tid == 0 && bad_s) flag_nonfinite(P, it.tensor);
 }
 
+// VEC tiles through a per-warp double buffer filled by cp.async (LDGSTS):
+// every lane copies, and later reads back, only its own 16-byte column
+// groups, so a lane waits on its own copy groups (no cross-lane sync) while
+// the next row pair is already in flight -- twice the bytes in flight of the
+// register-staged loop without registers to hold them.
+constexpr int kFactorBufs = 2;
+struct FactorSmem {
+  double colbuf[kFactorWarps][kStripCols];
+  float4 rows[kFactorWarps][kFactorBufs][2][kStripCols / 4];
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ void factor_tile_async(const DevicePlan &P, const FactorItem &it, const TensorDesc &T,
+                                  FactorSmem &F) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ uint32_t bad_s;
+  if (tid == 0) bad_s = 0;
+  double colacc[16];
+#pragma unroll
+  for (int k = 0; k < 16; k++) colacc[k] = 0.0;
+  const int64_t n = T.n, width = it.b1 - it.b0;
+  // row pairs of this warp: (a0 + warp + 16 q, a0 + warp + 16 q + 8)
+  const int64_t first = it.a0 + warp;
+  const int npairs = first < it.a1 ? (int)((it.a1 - first + 2 * kFactorWarps - 1) / (2 * kFactorWarps)) : 0;
+  auto issue = [&](int q) {
+    const int buf = q % kFactorBufs;
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+      const int64_t row = first + (int64_t)q * 2 * kFactorWarps + r * kFactorWarps;
+      if (row < it.a1) {
+        const float *g = T.grad + row * n + it.b0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int b = 4 * lane + 128 * k;
+          if (b < width) cp_async16(&F.rows[warp][buf][r][lane + 32 * k], g + b);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  bool bad = false;
+  if (npairs > 0) issue(0);
+  for (int q = 0; q < npairs; q++) {
+    if (q + 1 < npairs) {
+      issue(q + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    const int buf = q % kFactorBufs;
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+      const int64_t row = first + (int64_t)q * 2 * kFactorWarps + r * kFactorWarps;
+      if (row >= it.a1) break;
+      float v[16];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int b = 4 * lane + 128 * k;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (b < width) x = F.rows[warp][buf][r][lane + 32 * k];
+        v[4 * k + 0] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
+      }
+      const bool full = row * n >= T.lo && (row + 1) * n <= T.hi;
+      double rowp2[2] = {0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < 16; k++) {
+        double sq = (double)v[k] * (double)v[k];
+        if (!full) {
+          const int64_t e = row * n + col_of<true>(it.b0, lane, k);
+          if (e < T.lo || e >= T.hi) sq = 0.0;
+        }
+        colacc[k] += sq;
+        rowp2[k & 1] += sq;
+      }
+      const double rowp = warp_sum(rowp2[0] + rowp2[1]);
+      if (lane == 0) {
+        T.rowpart[(int64_t)it.strip * T.m + row] = rowp;
+        bad |= !isfinite(rowp);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 16; k++) F.colbuf[warp][(int)col_of<true>(0, lane, k)] = colacc[k];
+  __syncthreads();
+  for (int64_t j = tid; j < width; j += kFactorThreads) {
+    double c = F.colbuf[0][j];
+#pragma unroll
+    for (int w = 1; w < kFactorWarps; w++) c += F.colbuf[w][j];
+    T.colpart[(int64_t)it.rowblock * n + it.b0 + j] = c;
+  }
+  if (bad) atomicOr(&bad_s, 1u);
+  __syncthreads();
+  if (tid == 0 && bad_s) flag_nonfinite(P, it.tensor);
+}
+
 // Vector (m, 1): the row sum of row a is g[a]^2; the single column sums all
 // rows.  Four rows per thread per step, loads first.
 __device__ void factor_vector(const DevicePlan &P, const FactorItem &it, const TensorDesc &T) {
@@ -154,16 +260,17 @@ __device__ void factor_vector(const DevicePlan &P, const FactorItem &it, const T
 
 // One CTA per item (the loop also allows a persistent launch).
 __global__ void __launch_bounds__(kFactorThreads, 2) factor_partials_kernel(DevicePlan P) {
-  __shared__ double colbuf[kFactorWarps][kStripCols];   // one copy for both tile variants
+  extern __shared__ __align__(16) unsigned char factor_smem_raw[];
+  FactorSmem &F = *reinterpret_cast<FactorSmem *>(factor_smem_raw);
   for (int item = blockIdx.x; item < P.n_factor_items; item += gridDim.x) {
     const FactorItem it = P.factor_items[item];
     const TensorDesc T = P.tensors[it.tensor];
     if (T.n == 1) {
       factor_vector(P, it, T);
     } else if ((T.n & 3) == 0 && (reinterpret_cast<uintptr_t>(T.grad) & 15) == 0) {
-      factor_tile<true>(P, it, T, colbuf);
+      factor_tile_async(P, it, T, F);
     } else {
-      factor_tile<false>(P, it, T, colbuf);
+      factor_tile<false>(P, it, T, F.colbuf);
     }
     __syncthreads();   // shared scratch is reused by the next item
   }
@@ -308,7 +415,14 @@ void launch_factor_partials(const DevicePlan &P, cudaStream_t s) {
   // one CTA per item (measured faster than a persistent grid: items differ in
   // size, and short CTAs backfill)
   (void)g_factor_sms;
-  if (P.n_factor_items > 0) factor_partials_kernel<<<P.n_factor_items, kFactorThreads, 0, s>>>(P);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(factor_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(FactorSmem));
+    attr = true;
+  }
+  if (P.n_factor_items > 0)
+    factor_partials_kernel<<<P.n_factor_items, kFactorThreads, sizeof(FactorSmem), s>>>(P);
 }
 
 void launch_factor_reduce(const DevicePlan &P, int64_t max_mn, cudaStream_t s) {
