@@ -374,20 +374,19 @@ __device__ __forceinline__ void wd_wait(uint64_t *bar, uint32_t parity, int tag,
 #define WAIT(bar, par, tag) tc::mbar_wait(bar, par)
 #endif
 
-// Ring position of a role that takes every STEP-th tile.
-template <int N, int STEP>
-struct Stride {
+// Ring / slot position of tile t, computed directly (a power-of-two ring is
+// two bit operations, the 6-slot TMEM ring a multiply-high): cheaper than
+// carrying wrap-around cursors through the loop.
+template <int N>
+struct Pos {
   int i;
-  uint32_t phase = 0;
-  bool wrapped = false;
-  __device__ __forceinline__ explicit Stride(int start) : i(start) {}
-  __device__ __forceinline__ void next() {
-    i += STEP;
-    if (i >= N) {
-      i -= N;
-      phase ^= 1u;
-      wrapped = true;
-    }
+  uint32_t phase;
+  bool wrapped;
+  __device__ __forceinline__ explicit Pos(int32_t t) {
+    const uint32_t u = (uint32_t)t;
+    i = (int)(u % (uint32_t)N);
+    phase = (u / (uint32_t)N) & 1u;
+    wrapped = u >= (uint32_t)N;
   }
 };
 
@@ -505,9 +504,9 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     const uint32_t one = tbase + kOneCol;
     // layer-1 slices are N = 32 rows (LBO 512 B), layer-2 slices N = 48 (LBO 768 B)
     const uint64_t dimg0 = tc::smem_desc_kmajor(tc::smem_u32(&S.img[0]), l1 ? 512 : kN2 * 16, 128);
-    Cursor<kRing> rc;
-    Cursor<kSlots> sc;
     for (int32_t i = 0; i < nt; i++) {
+      const Pos<kRing> rc(i);
+      const Pos<kSlots> sc(i);
       WAIT(l1 ? &S.op_ready[sc.i] : &S.h_ready[sc.i], sc.phase, 4);
       tc::fence_after_sync();
       trace(P, i, l1 ? 3 : 5);
@@ -519,8 +518,6 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
         else issue_layer2(dimg, op, acc, one, &S.acc2_full[sc.i]);
       }
       __syncwarp();
-      rc.next();
-      sc.next();
     }
   } else if (warp < kWarpB) {
     // ------------------------------------------ WG_A: features -> E/B operands
@@ -531,9 +528,9 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     int32_t col_j = -1, col_b0 = -1;   // rowblock: cached column entry of this lane
     int32_t a_img = -1, a_par = -1;    // operand image last waited for
     Entry ce;
-    Stride<kRing, kStep> rc(r0);
-    Stride<kSlots, kStep> sc(r0);
     for (int32_t i = r0; i < nt; i += kStep) {
+      const Pos<kRing> rc(i);
+      const Pos<kSlots> sc(i);
       WAIT(&S.full[rc.i], rc.phase, 5);
       if (warp == 0) trace(P, i, 1);
       const Stage &st = S.stage[rc.i];
@@ -618,15 +615,13 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       tc::fence_before_sync();
       if (warp == 0) trace(P, i, 2);
       warp_arrive(&S.op_ready[sc.i]);
-      rc.next();
-      sc.next();
     }
   } else if (warp < kWarpC) {
     // ------------------------------------------- WG_B: layer-1 epilogue -> H
     const int r0 = (warp - kWarpB) >> 2;
     constexpr int kStep = kWGsB;
-    Stride<kSlots, kStep> sc(r0);
     for (int32_t i = r0; i < nt; i += kStep) {
+      const Pos<kSlots> sc(i);
       // B touches neither the data ring nor the operand image (the layer-1
       // scale 2^-s2 is folded into W1): it waits for the accumulator only
       if (warp == kWarpB) trace(P, i, 10);
@@ -649,7 +644,6 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       tc::tmem_st_wait();
       tc::fence_before_sync();
       warp_arrive(&S.h_ready[sc.i]);
-      sc.next();
     }
   } else if (warp < kWarpProducer) {
     // ------------------------- WG_C: layer-2 epilogue, layer 3, update, store
@@ -661,9 +655,9 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
     const int n_peers = P.n_peers;
     int red_j = -1;
     float red_max = 0.0f, red_out = 0.0f;   // max |delta|, NaN-propagating max |theta'|
-    Stride<kRing, kStep> rc(r0);
-    Stride<kSlots, kStep> sc(r0);
     for (int32_t i = r0; i < nt; i += kStep) {
+      const Pos<kRing> rc(i);
+      const Pos<kSlots> sc(i);
       WAIT(&S.full[rc.i], rc.phase, 5);
       const Stage &st = S.stage[rc.i];
       const TileMeta &mt = st.meta;
@@ -739,8 +733,6 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
           *reinterpret_cast<float *>(reinterpret_cast<char *>(tp) + P.peer_delta[q]) = out;
       }
       if (warp == kWarpC) trace(P, i, 7);
-      rc.next();
-      sc.next();
     }
     if (red_j >= 0) {
       if (red_max > 0.0f)
