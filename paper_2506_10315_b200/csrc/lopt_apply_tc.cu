@@ -681,16 +681,17 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
       WAIT(&S.acc2_full[sc.i], sc.phase, 8);
       tc::fence_after_sync();
       if (warp == kWarpC) trace(P, i, 6);
-      // layer 3 in f32: b3 + linear half (from the MMA) + sum (w3/2)|h2|,
-      // four independent FFMA2 chains, |x| as an operand modifier (no ReLU
-      // pass); h2 is read in two 16-column halves to stay within 72 registers
+      // layer 3 in f32: (b3 + linear half, from the MMA) + sum (w3/2)|h2| as
+      // {dir, mag} pairs -- |h2[j]| is a broadcast operand with the |x|
+      // modifier, two chains (even / odd j); h2 is read in two 16-column
+      // halves to stay within the register budget
       const uint32_t tc2 = tbase + lane_addr + kSlotCols * sc.i + 32;
       uint32_t h2[16], lin[2];
       tc::tmem_ld16(tc2, h2);
       tc::tmem_ld2(tc2 + 32, lin);
       tc::tmem_ld_wait();
-      float2 d0 = make_float2(ip.b3[0] + __uint_as_float(lin[0]), 0.0f), d1 = make_float2(0.0f, 0.0f);
-      float2 m0 = make_float2(ip.b3[1] + __uint_as_float(lin[1]), 0.0f), m1 = make_float2(0.0f, 0.0f);
+      float2 de = make_float2(__uint_as_float(lin[0]), __uint_as_float(lin[1]));
+      float2 dd = make_float2(0.0f, 0.0f);
       const float4 *w3 = reinterpret_cast<const float4 *>(ip.w3h);
 #pragma unroll
       for (int half = 0; half < 2; half++) {
@@ -701,16 +702,11 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
           warp_arrive(&S.slot_free[sc.i]);
         }
 #pragma unroll
-        for (int q = 0; q < 8; q += 2) {
-          const float4 wa = w3[8 * half + q], wb = w3[8 * half + q + 1];
-          const float2 ha = make_float2(fabsf(__uint_as_float(h2[2 * q])),
-                                        fabsf(__uint_as_float(h2[2 * q + 1])));
-          const float2 hb = make_float2(fabsf(__uint_as_float(h2[2 * q + 2])),
-                                        fabsf(__uint_as_float(h2[2 * q + 3])));
-          d0 = ffma2(ha, make_float2(wa.x, wa.y), d0);
-          m0 = ffma2(ha, make_float2(wa.z, wa.w), m0);
-          d1 = ffma2(hb, make_float2(wb.x, wb.y), d1);
-          m1 = ffma2(hb, make_float2(wb.z, wb.w), m1);
+        for (int q = 0; q < 8; q++) {
+          const float4 w = w3[8 * half + q];
+          const float he = fabsf(__uint_as_float(h2[2 * q])), ho = fabsf(__uint_as_float(h2[2 * q + 1]));
+          de = ffma2(make_float2(he, he), make_float2(w.x, w.y), de);
+          dd = ffma2(make_float2(ho, ho), make_float2(w.z, w.w), dd);
         }
       }
       // the data slot (theta, meta) and the image are no longer needed
@@ -719,7 +715,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
         asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&S.c_done[r0][warp & 3])),
                      "r"(i)
                      : "memory");
-      const float dir = (d0.x + d0.y) + (d1.x + d1.y), mag = (m0.x + m0.y) + (m1.x + m1.y);
+      const float dir = de.x + dd.x, mag = de.y + dd.y;
       // engine.py:537-539, exp on the SFU (fp32 tolerance path)
       const float du = dsb * (dir * ex2_ftz(mag * alpha_log2e));
       const float out = (w + du) * decay;   // optim.py:100-101 (decay = 1 without weight decay)

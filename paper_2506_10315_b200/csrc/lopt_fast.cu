@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
   // layer 2: [W2 | v] hi/lo by K halves, then the bias slice (k = 0: hi, k = 1: lo).
   // Rows 32/33 carry the linear half of layer 3 (see PrepImage): v_out[k] =
   // 1/2 * 2^s2 * sum_o w3[out,o] W2[o,k] (its input is relu(h1) * 2^-s2) and the
-  // bias 1/2 * sum_o w3[out,o] b2[o]; summed in f64, rounded once.
+  // bias 1/2 * sum_o w3[out,o] b2[o] + b3[out]; summed in f64, rounded once.
   const float sd = s2s[0], su = s2s[1];
   __shared__ float vrow[2][32], vbias[2];
   if (threadIdx.x < 64) {
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
     const int out = threadIdx.x - 64;
     double acc = 0.0;
     for (int o = 0; o < 32; o++) acc += (double)w3[out * 32 + o] * (double)b2[o];
-    vbias[out] = (float)(0.5 * acc);
+    vbias[out] = (float)(0.5 * acc + (double)b3[out]);   // b3 rides along
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kN2 * 32; i += blockDim.x) {
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
   }
   if (threadIdx.x < 64) {
     const int o = threadIdx.x & 31, out = threadIdx.x >> 5;
-    img->w3h[o >> 1][2 * out + (o & 1)] = w3[out * 32 + o] * su * 0.5f;
+    img->w3h[o >> 1][2 * (o & 1) + out] = w3[out * 32 + o] * su * 0.5f;
   }
   if (threadIdx.x < 2) img->b3[threadIdx.x] = b3[threadIdx.x];
   if (threadIdx.x < 3) img->sqmr[threadIdx.x] = sqrtf(P.tscal[j].mr[threadIdx.x]);

@@ -31,7 +31,7 @@ constexpr int kTile = 128;
 // Layer 3 without a ReLU pass: relu(h) = (h + |h|)/2, so
 //   dir = b3 + 1/2 sum_o w3[o] h2[o] + 1/2 sum_o w3[o] |h2[o]|.
 // The linear half is linear in relu(h1), so it rides on the layer-2 MMAs as
-// two extra output rows v = 1/2 W2^T w3 (bias 1/2 w3.b2): layer 2 runs with
+// two extra output rows v = 1/2 W2^T w3 (bias 1/2 w3.b2 + b3): layer 2 runs with
 // N = 48 (rows 32, 33 = dir, mag; 34..47 zero) and the epilogue only forms
 // sum (w3/2) |h2| with FFMA2's |x| operand modifier.
 //
@@ -45,7 +45,7 @@ constexpr int kN2 = 48;     // layer-2 MMA width: 32 hidden + {dir, mag} linear 
 struct __align__(128) PrepImage {
   uint16_t b1[4][512];      // W1 over E: hi, lo; W1 over B: hi, lo
   uint16_t b2[5][kN2 * 16]; // [W2|v]_hi[K0-15], _hi[K16-31], _lo[K0-15], _lo[K16-31], bias
-  float w3h[16][4];         // {w3d[2q], w3d[2q+1], w3m[2q], w3m[2q+1]} * 2^s2 / 2
+  float w3h[16][4];         // {w3d[2q], w3m[2q], w3d[2q+1], w3m[2q+1]} * 2^s2 / 2
   float escale[20];         // normalization scale of the per-element columns (+ clip), float4-read
   float b3[2];
   float sqmr[3];            // sqrt(mean r_i)
