@@ -161,10 +161,24 @@ def make_model(workload, device, seed=0):
     return params, grads
 
 
-def build_optimizer(params, feature_set, mode, world, strategy="range"):
+def workload_hparams(workload):
+    """BASELINE.json config 5: GPT-2 medium runs with a cosine LR schedule and
+    weight decay 0.01; the others at constant lr 1, no decay.
+    (Same kernels either way: decay is one multiply, the schedule a host scalar.)"""
+    if workload == "gpt2_medium":
+        from paper_2506_10315_b200 import ScheduleConfig
+
+        return {"weight_decay": 0.01,
+                "schedule": ScheduleConfig(kind="cosine", max_lr=1.0, min_lr=0.1,
+                                           warmup_steps=2, total_steps=10_000)}
+    return {}
+
+
+def build_optimizer(params, feature_set, mode, world, strategy="range", hp=None):
     """feature_set "velo" is the full VeLO optimizer (VELO_MLP features + the
     per-tensor LSTM hypernetwork mixing a bank of MLPs); "small_fc_lopt" and
     "velo_mlp" are the single-MLP learned optimizers."""
+    hp = hp or {}
     # N > 1: the parameter exchange is fused into the apply kernel (stores to
     # the peers' IPC-mapped arenas over NVLink) unless LOPT_GATHER=nccl
     gather = os.environ.get("LOPT_GATHER", "p2p" if mode == "fast" else "nccl")
@@ -174,26 +188,27 @@ def build_optimizer(params, feature_set, mode, world, strategy="range"):
 
             try:
                 return ShardedVeLO(params, mode=mode, check_errors=False, gather=gather,
-                                   strategy=strategy)
+                                   strategy=strategy, **hp)
             except Exception as e:  # noqa: BLE001
                 print(f"bench: p2p gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
-                return ShardedVeLO(params, mode=mode, check_errors=False, strategy=strategy)
+                return ShardedVeLO(params, mode=mode, check_errors=False, strategy=strategy, **hp)
         from paper_2506_10315_b200.velo import VeLO_CUDA
 
-        return VeLO_CUDA(params, mode=mode, check_errors=False)
+        return VeLO_CUDA(params, mode=mode, check_errors=False, **hp)
     if world > 1:
         from paper_2506_10315_b200.dist import ShardedLearnedOptimizer
 
         try:
             return ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
-                                           check_errors=False, gather=gather, strategy=strategy)
+                                           check_errors=False, gather=gather, strategy=strategy,
+                                           **hp)
         except Exception as e:  # noqa: BLE001
             print(f"bench: p2p gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
             return ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
-                                           check_errors=False, strategy=strategy)
+                                           check_errors=False, strategy=strategy, **hp)
     from paper_2506_10315_b200 import LearnedOptimizer
 
-    return LearnedOptimizer(params, feature_set=feature_set, mode=mode, check_errors=False)
+    return LearnedOptimizer(params, feature_set=feature_set, mode=mode, check_errors=False, **hp)
 
 
 def step_kwargs(opt):
@@ -449,7 +464,8 @@ def main():
     dev = torch.device("cuda", torch.cuda.current_device())
     params, grads = make_model(args.workload, dev, seed=0)
 
-    opt = build_optimizer(params, args.feature_set, args.mode, world, args.strategy)
+    hp = workload_hparams(args.workload)
+    opt = build_optimizer(params, args.feature_set, args.mode, world, args.strategy, hp)
     gather_used = getattr(opt, "gather", "nccl")
     clk = ClockSampler(torch.cuda.current_device())
     clk.__enter__()   # sampled through the timed steps, the phase pass and the e2e run
@@ -501,7 +517,7 @@ def main():
         del opt
         torch.cuda.empty_cache()
         params, grads = make_model(args.workload, dev, seed=0)
-        vopt = build_optimizer(params, "velo", args.mode, world, args.strategy)
+        vopt = build_optimizer(params, "velo", args.mode, world, args.strategy, hp)
         vms, vph, _ = time_device(vopt, params, grads, args.steps, args.warmup, world)
         velo = {"optimizer": "VeLO_CUDA (VELO_MLP features + per-tensor LSTM hypernetwork, "
                              "bank of 4 MLPs)",
@@ -566,6 +582,8 @@ def main():
             "scaling": "strong" if world > 1 else "none", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": args.workload, "feature_set": args.feature_set,
+                       "hparams": ({k: (repr(v) if k == "schedule" else v) for k, v in hp.items()}
+                                   or {"lr": 1.0, "weight_decay": 0.0}),
                        "mode": args.mode, "tensors": n_tensors, "params": n_params,
                        "parallelism": (("element-sharded" if args.strategy == "range" else
                                         "tensor-owner-sharded") + f" x{world}, param exchange "
