@@ -253,3 +253,72 @@ def test_backward_overlapped_reduce_scatter_step_bitwise():
         assert nb > 1
         for a, b in zip(out, single):
             assert a.tobytes() == b.tobytes()
+
+
+def _velo_worker(rank, world, port, mode, strategy, q):
+    import sys
+    import traceback
+
+    sys.path.insert(0, ROOT)
+    try:
+        import torch
+        import torch.distributed as dist
+
+        from paper_2506_10315_b200.dist import ShardedVeLO
+
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        init, grads = _init()
+        params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+        opt = ShardedVeLO(params, mode=mode, weight_decay=0.01, strategy=strategy)
+        for k, gs in enumerate(grads):
+            for p, g in zip(params, gs):
+                p.grad = torch.from_numpy(g).cuda()
+            opt.step(loss=2.5 - 0.1 * k)
+        torch.cuda.synchronize()
+        q.put((rank, [p.detach().cpu().numpy().copy() for p in params]))
+        dist.destroy_process_group()
+    except Exception:
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("mode,strategy", [("strict", "range"), ("strict", "owner"),
+                                           ("fast", "range")])
+def test_sharded_velo_equals_single_gpu(mode, strategy):
+    """The full VeLO optimizer sharded over two ranks: every rank runs the
+    per-tensor LSTM on the merged statistics, so all ranks mix the same MLPs
+    and the result equals VeLO_CUDA on one GPU (bitwise in strict mode)."""
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_2506_10315_b200 as P
+
+    init, grads = _init()
+    params = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    opt = P.VeLO_CUDA(params, mode=mode, weight_decay=0.01)
+    for k, gs in enumerate(grads):
+        for p, g in zip(params, gs):
+            p.grad = torch.from_numpy(g).cuda()
+        opt.step(loss=2.5 - 0.1 * k)
+    single = [p.detach().cpu().numpy() for p in params]
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_velo_worker, args=(r, 2, port, mode, strategy, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, out in res:
+        assert not isinstance(out, str), out
+        for a, b in zip(out, single):
+            if mode == "strict":
+                assert a.tobytes() == b.tobytes()
+            else:
+                err = np.abs(a.astype(np.float64) - b) / (1 + np.abs(b))
+                assert err.max() <= 1e-6, err.max()
