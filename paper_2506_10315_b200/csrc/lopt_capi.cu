@@ -38,8 +38,23 @@ using namespace lopt;
 
 namespace {
 
-constexpr int64_t kStrictStatChunk = 8192;
-constexpr int64_t kStrictApplyChunk = 4096;
+// strict-mode item sizes; LOPT_STRICT_CHUNKS="stat,apply" overrides them for
+// tuning sweeps
+int64_t strict_chunk(int which) {
+  static int64_t v[2] = {0, 0};
+  if (v[0] == 0) {
+    v[0] = 8192;
+    v[1] = 65536;   // 65536: -2 % vs 4096 (fewer per-item MLP smem fills)
+    if (const char *e = getenv("LOPT_STRICT_CHUNKS")) {
+      long long a = 0, b = 0;
+      if (sscanf(e, "%lld,%lld", &a, &b) == 2 && a >= 256 && b >= 512) {
+        v[0] = a;
+        v[1] = b;
+      }
+    }
+  }
+  return v[which];
+}
 // elements per factor CTA (rows x <=512 columns); LOPT_FACTOR_TILE overrides
 // it for tuning sweeps
 int64_t factor_tile_elems() {
@@ -123,8 +138,8 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   p->descs.resize(count);
   const int D = d_feat(cfg->feature_set);
   const bool fast = cfg->mode == LOPT_MODE_FAST;
-  const int64_t stat_chunk = fast ? fast_stat_chunk() : kStrictStatChunk;
-  const int64_t apply_chunk = fast ? fast_apply_chunk() : kStrictApplyChunk;
+  const int64_t stat_chunk = fast ? fast_stat_chunk() : strict_chunk(0);
+  const int64_t apply_chunk = fast ? fast_apply_chunk() : strict_chunk(1);
   int64_t rowpart = 0, colpart = 0, rows = 0, cols = 0;
   for (int j = 0; j < count; j++) {
     const lopt_tensor &t = tensors[j];
