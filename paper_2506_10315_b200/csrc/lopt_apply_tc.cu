@@ -2,8 +2,9 @@
 //
 // engine.py:657-710 fused_apply + state.py:77-90 + optim.py:171-172 for
 // 128-element tiles: features -> layer 1 (tcgen05, M=128 elements) -> ReLU ->
-// layer 2 (tcgen05) -> ReLU -> layer 3 (CUDA cores, f32) -> exp -> update ->
-// decay -> store theta and the advanced accumulators.
+// layer 2 (tcgen05, plus the linear half of layer 3 as two extra output rows)
+// -> layer 3's |h2| half (CUDA cores, f32; relu(x) = (x + |x|)/2) -> exp ->
+// update -> decay -> store theta and the advanced accumulators.
 //
 // fp32 accuracy on the f16 tensor-core path: every operand is split in two
 // fp16 terms and each product is x_hi*W_hi + x_lo*W_hi + x_hi*W_lo with f32
@@ -12,7 +13,7 @@
 // Structure: a warp-specialized persistent kernel, one CTA per SM, that
 // streams the CTA's contiguous range of tiles through a pipeline:
 //
-//   producer warp  --TMA bulk copies-->  smem ring of kRing tile slots
+//   producer warps --TMA bulk copies-->  smem ring of kRing tile slots
 //                  (theta, g, {M1,M2,M3,V} quads, row-table entry, and the
 //                   tensor's operand image when the tensor changes)
 //   WG_A (128 thr) features -> E/B operands in TMEM slot   --op_ready-->
@@ -21,8 +22,10 @@
 //   MMA warp L2    7 x tcgen05.mma (N = 48) -> acc         --acc2_full-->
 //   WG_C (128 thr) layer 3 (|h2| FFMA2s + MMA linear half), exp, update, store theta --slot_free/data_free-->
 //
-// Thread i of each warpgroup owns TMEM lane i = lane i of every tile.  TMEM
-// holds kSlots tiles in flight (kSlotCols = 80 columns each: 32 operand, 48 accumulator), so
+// Each role has two warpgroups taking alternate tiles; ring and TMEM-slot
+// positions are computed from the tile index (Pos).  Thread i of a warpgroup
+// owns TMEM lane i = lane i of its tiles.  TMEM holds kSlots tiles in flight
+// (kSlotCols = 80 columns each: 32 operand, 48 accumulator), so
 // MMA latency is hidden by the other tiles' CUDA-core work instead of being
 // waited out.  All hand-offs are mbarriers; MMAs are issued by one elected
 // lane of a converged warp (descriptors in uniform registers, back-to-back
