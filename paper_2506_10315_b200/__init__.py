@@ -12,9 +12,10 @@ from .velo import VeLO_CUDA, VeLOHyperNet
 from .weights import BetaConfig, LoptWeights, random_weights, zero_weights
 
 __all__ = [
-    "AdafacLO_CUDA", "BetaConfig", "DeviceOptState", "EngineError", "FeatureSet",
-    "FeatureSetSpec", "LearnedOptimizer", "LoptWeights", "OptimError", "ScheduleConfig", "Slot",
-    "StepPlan", "UpdateOverflowError", "column_names", "FeatureStats", "fused_apply", "fused_stats", "random_weights",
-    "schedule_lr", "small_fc_lopt_spec", "spec_by_name", "step_fused", "step_naive", "time_features",
-    "velo_mlp_spec", "view_2d", "zero_weights",
+    "AdafacLO_CUDA", "BetaConfig", "column_names", "DeviceOptState", "EngineError",
+    "fast_available", "FeatureSet", "FeatureSetSpec", "FeatureStats", "fused_apply",
+    "fused_stats", "LearnedOptimizer", "LoptWeights", "OptimError", "random_weights",
+    "schedule_lr", "ScheduleConfig", "Slot", "small_fc_lopt_spec", "spec_by_name",
+    "step_fused", "step_naive", "StepPlan", "time_features", "UpdateOverflowError",
+    "VeLO_CUDA", "velo_mlp_spec", "VeLOHyperNet", "view_2d", "zero_weights",
 ]
