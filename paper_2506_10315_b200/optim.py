@@ -347,18 +347,28 @@ class LearnedOptimizer(torch.optim.Optimizer):
             comp.wait_event(uploaded[gi])
             ps = [params[k] for k in ks]
             plan = hs["plans"][b][gi]
-            slots = [self._slot(p) for p in ps]
+            hkey = ("host", gi)
+            weights, widx = self._weights_for_group(hkey, ps)
+            slots = [self._slot(p, w) for p, w in zip(ps, widx)]
             for k, sl in zip(ks, slots):
                 sl.grad = garena[offs[k]:offs[k + 1]]
             ptrs = [(sl.theta.data_ptr(), sl.grad.data_ptr()) for sl in slots]
             if plan is None:
-                plan = StepPlan(slots, self.spec, self.lopt_weights, mode=self.mode)
+                plan = StepPlan(slots, self.spec, weights, mode=self.mode)
                 hs["plans"][b][gi] = plan
                 hs["ptrs"][b][gi] = ptrs
             elif hs["ptrs"][b][gi] != ptrs:
                 plan.rebind(slots)
                 hs["ptrs"][b][gi] = ptrs
-            plan.step(lr, wd, t)
+            if self._after_stats is None:
+                plan.step(lr, wd, t)
+            else:   # VeLO: the per-tensor hypernetwork between phases 1 and 2
+                plan.set_step(lr, wd, t)
+                plan.factor_partials()
+                plan.factor_finalize()
+                plan.feature_stats()
+                self._after_stats(hkey, plan, ps)
+                plan.apply()
             launched.append((plan, ps))
             if host_params is not None:
                 done = torch.cuda.Event()

@@ -133,3 +133,10 @@ class VeLO_CUDA(_VeLOMixin, LearnedOptimizer):
                 loss = closure()
         self._set_loss(loss)
         return super().step(loss=loss)
+
+    def step_host(self, host_grads, host_params=None, *, chunks: int = 8, loss=None):
+        """LearnedOptimizer.step_host with the loss VeLO's hypernetwork needs;
+        each tensor group runs the hypernetwork between its phases 1 and 2
+        (per-tensor LSTM state kept per group: do not alternate with step())."""
+        self._set_loss(loss)
+        return super().step_host(host_grads, host_params, chunks=chunks)

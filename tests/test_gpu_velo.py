@@ -103,3 +103,34 @@ def test_velo_requires_loss():
     p.grad = torch.ones(4, 4, device="cuda")
     with pytest.raises(P.OptimError):
         opt.step()
+
+
+def test_velo_step_host_matches_device_step():
+    """VeLO through the host-buffer step (tensor groups, each running the
+    hypernetwork between its phases) equals VeLO_CUDA.step on device-resident
+    gradients bit for bit: the per-tensor LSTM and the per-element kernels do
+    not depend on how tensors are grouped."""
+    import torch
+
+    import paper_2506_10315_b200 as P
+
+    shapes = [(128, 784), (128,), (10, 128), (10,), (33, 70)]
+    rng = np.random.default_rng(13)
+    init = [np.asarray(rng.standard_normal(s) * 0.02, dtype=np.float32) for s in shapes]
+    grads = [[np.asarray(rng.standard_normal(s) * 1e-3, dtype=np.float32) for s in shapes]
+             for _ in range(3)]
+    a = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    b = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    oa = P.VeLO_CUDA(a, mode="fast", weight_decay=0.01)
+    ob = P.VeLO_CUDA(b, mode="fast", weight_decay=0.01)
+    host_p = [torch.empty(s, dtype=torch.float32).pin_memory() for s in shapes]
+    for k, gs in enumerate(grads):
+        for p, g in zip(a, gs):
+            p.grad = torch.from_numpy(g).cuda()
+        oa.step(loss=2.0 - 0.1 * k)
+        ob.step_host([torch.from_numpy(g).pin_memory() for g in gs], host_p, chunks=2,
+                     loss=2.0 - 0.1 * k)
+    torch.cuda.synchronize()
+    for p, q, h in zip(a, b, host_p):
+        assert p.detach().cpu().numpy().tobytes() == q.detach().cpu().numpy().tobytes()
+        assert h.numpy().tobytes() == q.detach().cpu().numpy().tobytes()
