@@ -318,6 +318,13 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
             self._finish_grad_reduce()
         return super().step(closure=closure, loss=loss)
 
+    def step_host(self, *args, **kw):
+        """Not for the sharded optimizer: its parameters live in the shared
+        arena the exchange writes into.  Copy each rank's slice in and out
+        around step() instead (what bench.py's sharded e2e does)."""
+        raise NotImplementedError("step_host is single-GPU; copy flat_grads()/flat slices "
+                                  "around step() on each rank")
+
     def _slot(self, p, weight_slot=0) -> Slot:
         s = super()._slot(p, weight_slot)
         s.lo, s.hi = self.state[p]["range"]
