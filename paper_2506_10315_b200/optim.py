@@ -443,6 +443,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
                     st[k] = st[k].to(torch.float32).contiguous()
         self.T = int(extra.get("T", self.T))
         self._plans.clear()
+        self._host_step = None   # its plans point at the replaced state tensors
 
 
 class AdafacLO_CUDA(LearnedOptimizer):

@@ -79,12 +79,29 @@ class _VeLOMixin:
     def _lstm_state(self, gi, params):
         st = self._lstm.get(gi)
         if st is None or st.shape[0] != len(params):
+            # one contiguous [tensors x 2H] block per group for the kernel;
+            # rows start from the tensors' current LSTM state (a resumed or
+            # regrouped optimizer continues where it was)
             dev = params[0].device
             st = torch.zeros(len(params), 2 * self.hypernet.H, dtype=torch.float32, device=dev)
-            self._lstm[gi] = st
             for j, p in enumerate(params):
+                prev = self.state[p].get("lstm")
+                if prev is not None:
+                    st[j].copy_(prev.to(device=dev, dtype=torch.float32).reshape(-1))
                 self.state[p]["lstm"] = st[j]
+            self._lstm[gi] = st
         return st
+
+    def state_dict(self):
+        sd = super().state_dict()
+        sd["velo"] = {"loss_ema": self._loss_ema}
+        return sd
+
+    def load_state_dict(self, state_dict):
+        extra = state_dict.get("velo", {})
+        super().load_state_dict({k: v for k, v in state_dict.items() if k != "velo"})
+        self._lstm = {}   # rebuilt from the loaded per-tensor rows on the next step
+        self._loss_ema = extra.get("loss_ema", self._loss_ema)
 
     def _set_loss(self, loss):
         if loss is None:

@@ -134,3 +134,42 @@ def test_velo_step_host_matches_device_step():
     for p, q, h in zip(a, b, host_p):
         assert p.detach().cpu().numpy().tobytes() == q.detach().cpu().numpy().tobytes()
         assert h.numpy().tobytes() == q.detach().cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_velo_state_dict_resume_is_bitwise(mode):
+    """VeLO checkpoint/resume: the per-tensor LSTM state and the loss EMA
+    travel in state_dict, so a fresh optimizer loaded mid-run continues the
+    trajectory bit for bit."""
+    import copy
+
+    import torch
+
+    import paper_2506_10315_b200 as P
+
+    shapes = [(64, 96), (64,), (10, 64), (10,)]
+    rng = np.random.default_rng(3)
+    init = [np.asarray(rng.standard_normal(s) * 0.02, dtype=np.float32) for s in shapes]
+    grads = [[np.asarray(rng.standard_normal(s) * 1e-3, dtype=np.float32) for s in shapes]
+             for _ in range(4)]
+    losses = [2.0, 1.8, 1.7, 1.5]
+
+    def run(opt, params, ks):
+        for k in ks:
+            for p, g in zip(params, grads[k]):
+                p.grad = torch.from_numpy(g).cuda()
+            opt.step(loss=losses[k])
+
+    a = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    oa = P.VeLO_CUDA(a, mode=mode)
+    run(oa, a, [0, 1])
+    sd = copy.deepcopy(oa.state_dict())
+    mid = [p.detach().clone() for p in a]
+    run(oa, a, [2, 3])
+    b = [torch.nn.Parameter(t.clone()) for t in mid]
+    ob = P.VeLO_CUDA(b, mode=mode)
+    ob.load_state_dict(sd)
+    run(ob, b, [2, 3])
+    torch.cuda.synchronize()
+    for p, q in zip(a, b):
+        assert p.detach().cpu().numpy().tobytes() == q.detach().cpu().numpy().tobytes()
