@@ -130,6 +130,9 @@ class LearnedOptimizer(torch.optim.Optimizer):
         return st
 
     def _slot(self, p, weight_slot=0) -> Slot:
+        if not p.is_cuda or p.grad is None or not p.grad.is_cuda:
+            raise TypeError("parameters and gradients must be CUDA tensors (the step runs "
+                            "on the device; use step_host for host-resident buffers)")
         st = self._init_state(p)
         m, n = view_2d(p.shape)
         if not p.is_contiguous():

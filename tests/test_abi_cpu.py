@@ -157,3 +157,17 @@ def test_packed_weight_layout():
     back = unpack(p, 39)
     for (a, b), (c, d) in zip(w.layers, back.layers):
         assert np.array_equal(a, c) and np.array_equal(b, d)
+
+
+def test_optimizer_rejects_host_tensors_before_any_device_call():
+    """CPU parameters would hand host pointers to the kernels: the optimizer
+    refuses them with a TypeError before building a plan."""
+    import torch
+
+    import paper_2506_10315_b200 as P
+
+    p = torch.nn.Parameter(torch.zeros(4, 3))
+    p.grad = torch.zeros(4, 3)
+    opt = P.LearnedOptimizer([p])
+    with pytest.raises(TypeError, match="CUDA"):
+        opt.step()
