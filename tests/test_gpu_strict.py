@@ -332,3 +332,31 @@ def test_range_operator_pair_matches_whole_tensor(P, oracle, spec_name, shape, m
     assert max(mx0, mx1) > 0
     with pytest.raises(P.EngineError):
         P.fused_apply(W, g, st, w, spec, a, out, lr=0.3, lo=0, hi=k, mode=mode)
+
+
+def test_torch_lr_scheduler_drives_group_lr(P):
+    """torch.optim.lr_scheduler works through param_groups[i]["lr"]: a
+    StepLR-halved run equals a run whose group lr is set by hand."""
+    import torch
+
+    shapes = [(32, 48), (32,)]
+    rng = np.random.default_rng(9)
+    init = [np.asarray(rng.standard_normal(s) * 0.05, dtype=F32) for s in shapes]
+    grads = [[np.asarray(rng.standard_normal(s) * 1e-2, dtype=F32) for s in shapes]
+             for _ in range(4)]
+    a = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    b = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    oa = P.LearnedOptimizer(a, lr=0.8, weight_decay=0.01)
+    ob = P.LearnedOptimizer(b, lr=0.8, weight_decay=0.01)
+    sched = torch.optim.lr_scheduler.StepLR(oa, step_size=2, gamma=0.5)
+    for k, gs in enumerate(grads):
+        for p, q, g in zip(a, b, gs):
+            p.grad = torch.from_numpy(g).cuda()
+            q.grad = torch.from_numpy(g).cuda()
+        ob.param_groups[0]["lr"] = 0.8 * (0.5 ** (k // 2))
+        oa.step()
+        ob.step()
+        sched.step()
+    for p, q in zip(a, b):
+        assert p.detach().cpu().numpy().tobytes() == q.detach().cpu().numpy().tobytes()
+    assert oa.param_groups[0]["lr"] == 0.8 * 0.25
