@@ -281,10 +281,19 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
                           "handles": []}
         for j, p in enumerate(ps):
             self._rs_hooks["handles"].append(
-                p.register_post_accumulate_grad_hook(lambda _p, j=j: self._grad_ready(j)))
+                p.register_post_accumulate_grad_hook(lambda q, j=j: self._grad_ready(j, q)))
 
-    def _grad_ready(self, j: int):
+    def _grad_ready(self, j: int, p=None):
         h = self._rs_hooks
+        if p is not None:
+            # a gradient that is not the arena view (e.g. after Module.zero_grad(),
+            # which sets grads to None) is moved into the arena before its
+            # bucket is reduced
+            off, n = self.offsets[j], p.numel()
+            view = self._flat_grad[off:off + n]
+            if p.grad is not None and p.grad.data_ptr() != view.data_ptr():
+                view.copy_(p.grad.reshape(-1))
+                p.grad = view.view(p.shape)
         b = h["bucket_of"][j]
         h["ready"][b] += 1
         if h["ready"][b] == len(self.buckets[b][2]) and b not in h["works"]:

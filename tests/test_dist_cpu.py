@@ -290,7 +290,7 @@ def _overlap_worker(rank, world, port, q):
         opt.overlap_grad_reduce(average=True)
         g = torch.Generator().manual_seed(10 + rank)
         x, y = torch.randn(4, 16, generator=g), torch.randn(4, 8, generator=g)
-        opt.zero_grad()
+        model.zero_grad()   # Module.zero_grad sets grads to None: the hooks re-home them
         torch.nn.functional.mse_loss(model(x), y).backward()
         launched = len(opt._rs_hooks["works"])   # buckets reduced during backward
         opt._finish_grad_reduce()
