@@ -219,14 +219,21 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         """The gradient arena: p.grad of every parameter becomes a view of it,
         laid out like the parameter arena (rank r's slice is its element
         range).  Backward accumulates local (unreduced) gradients into it."""
+        ps = self.param_groups[0]["params"]
         if getattr(self, "_flat_grad", None) is None:
-            ps = self.param_groups[0]["params"]
             self._flat_grad = torch.zeros_like(self.flat)
-            for p, off in zip(ps, self.offsets):
-                n = p.numel()
-                if p.grad is not None:
-                    self._flat_grad[off:off + n].copy_(p.grad.reshape(-1))
-                p.grad = self._flat_grad[off:off + n].view(p.shape)
+        for p, off in zip(ps, self.offsets):
+            # (re-)home gradients that are not arena views -- e.g. after
+            # Module.zero_grad() set them to None and backward made new ones
+            n = p.numel()
+            view = self._flat_grad[off:off + n]
+            if p.grad is None:
+                view.zero_()
+            elif p.grad.data_ptr() == view.data_ptr():
+                continue
+            else:
+                view.copy_(p.grad.reshape(-1))
+            p.grad = view.view(p.shape)
         return self._flat_grad
 
     def _bucket_rs(self, b: int, average: bool, async_op: bool):
