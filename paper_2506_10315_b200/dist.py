@@ -325,7 +325,18 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
             return
         super().zero_grad(set_to_none=set_to_none)
 
+    def _rehome_params(self):
+        """The exchange writes into the arena: parameters moved out of it (for
+        example by `p.data = ...`) are copied back and re-pointed."""
+        for p, off in zip(self.param_groups[0]["params"], self.offsets):
+            n = p.numel()
+            view = self.flat[off:off + n]
+            if p.data.data_ptr() != view.data_ptr():
+                view.copy_(p.data.reshape(-1))
+                p.data = view.view(p.shape)
+
     def step(self, closure=None, loss=None):
+        self._rehome_params()
         if self._rs_hooks is not None:
             if closure is not None:
                 with torch.enable_grad():
