@@ -268,6 +268,16 @@ class LearnedOptimizer(torch.optim.Optimizer):
         params = [p for g in self.param_groups for p in g["params"]]
         if len(self.param_groups) != 1:
             raise OptimError("step_host supports one parameter group")
+        # NumPy arrays (the reference's calling convention) are wrapped without
+        # a copy; pinned torch tensors give asynchronous transfers
+        host_grads = [torch.from_numpy(np.ascontiguousarray(g, dtype=np.float32))
+                      if isinstance(g, np.ndarray) else g for g in host_grads]
+        if host_params is not None:
+            for h in host_params:
+                if isinstance(h, np.ndarray) and (h.dtype != np.float32 or not h.flags.c_contiguous):
+                    raise OptimError("host parameter arrays must be C-contiguous float32")
+            host_params = [torch.from_numpy(h) if isinstance(h, np.ndarray) else h
+                           for h in host_params]
         if len(host_grads) != len(params):
             raise OptimError(f"got {len(host_grads)} gradients for {len(params)} tensors")
         if host_params is not None and len(host_params) != len(params):

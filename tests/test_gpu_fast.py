@@ -329,3 +329,26 @@ def test_fast_layer3_split_accuracy_with_skewed_hidden_layer(P, oracle, b2_shift
             worst = max(worst, _close(p.detach().cpu().numpy(), q))
     print(f"b2 shift {b2_shift}: max err/(1+|theta|) {worst:.3e}")
     assert worst <= TOL, worst
+
+
+def test_step_host_accepts_numpy_arrays(P):
+    """The reference's calling convention: gradients in, parameters out as
+    NumPy arrays (wrapped without a copy; synchronous transfers)."""
+    import torch
+
+    shapes = [(64, 96), (64,), (33, 70)]
+    rng = np.random.default_rng(17)
+    init = [np.asarray(rng.standard_normal(s) * 0.02, dtype=F32) for s in shapes]
+    grads = [np.asarray(rng.standard_normal(s) * 1e-3, dtype=F32) for s in shapes]
+    a = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    b = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    oa = P.LearnedOptimizer(a, mode="fast")
+    ob = P.LearnedOptimizer(b, mode="fast")
+    for p, g in zip(a, grads):
+        p.grad = torch.from_numpy(g).cuda()
+    oa.step()
+    out = [np.empty(s, F32) for s in shapes]
+    ob.step_host(grads, out, chunks=2)
+    torch.cuda.synchronize()
+    for p, h in zip(a, out):
+        assert p.detach().cpu().numpy().tobytes() == h.tobytes()
