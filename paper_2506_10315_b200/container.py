@@ -226,6 +226,14 @@ def checkpoint_save(opt, path, names=None) -> None:
     names = list(names) if names is not None else [f"t{k}" for k in range(len(ps))]
     if len(names) != len(ps):
         raise ValueError(f"{len(names)} names for {len(ps)} tensors")
+    if getattr(opt, "hypernet", None) is not None:
+        raise ValueError("the PYLO checkpoint layout has no VeLO hypernetwork state "
+                         "(optim.py:224-282); use opt.state_dict()")
+    for p in ps:
+        rng_ = opt.state.get(p, {}).get("range")
+        if rng_ is not None and tuple(rng_) != (0, p.numel()) and rng_[1] > rng_[0]:
+            raise ValueError("sharded optimizer state covers only this rank's element range; "
+                             "save per rank with state_dict() or gather it first")
     entries = {}
     for name, p in zip(names, ps):
         entries[f"param/{name}"] = p.detach().cpu().numpy().reshape(view_2d(p.shape))
