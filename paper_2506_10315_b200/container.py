@@ -231,7 +231,7 @@ def checkpoint_save(opt, path, names=None) -> None:
                          "(optim.py:224-282); use opt.state_dict()")
     for p in ps:
         rng_ = opt.state.get(p, {}).get("range")
-        if rng_ is not None and tuple(rng_) != (0, p.numel()) and rng_[1] > rng_[0]:
+        if rng_ is not None and tuple(rng_) != (0, p.numel()):
             raise ValueError("sharded optimizer state covers only this rank's element range; "
                              "save per rank with state_dict() or gather it first")
     entries = {}
