@@ -125,6 +125,15 @@ int lopt_factor_finalize(lopt_plan *plan, void *stream);
 int lopt_feature_stats(lopt_plan *plan, void *stream);
 int lopt_apply(lopt_plan *plan, void *stream);
 int lopt_step(lopt_plan *plan, const lopt_step_args *args, void *stream);
+/* The same step (including a registered VeLO hypernetwork) replayed from a
+ * CUDA graph captured on the first call: one launch per step instead of ~10,
+ * the step scalars patched into the graph's first kernel.  The capture holds
+ * the plan's device pointers; lopt_rebind_tensors / lopt_set_weights keep it
+ * valid (they rewrite device tables), lopt_set_peers / lopt_set_velo drop it.
+ * lopt_graph_reset drops it explicitly.  Replaces opt_step's per-step
+ * dispatch (optim.py:144-180) for a launch-bound caller. */
+int lopt_graph_step(lopt_plan *plan, const lopt_step_args *args, void *stream);
+int lopt_graph_reset(lopt_plan *plan);
 
 /* contiguous f64 blocks to all-reduce across element-sharded ranks */
 int lopt_factor_sums_ptr(lopt_plan *plan, double **ptr, int64_t *count);
@@ -149,6 +158,13 @@ int lopt_debug_ptrs(lopt_plan *plan, double **sumsq, float **factor_means);
 int lopt_velo_mix(lopt_plan *plan, const float *hyper, float *lstm_state, const float *bank,
                   const float *loss_feats, int32_t hidden, int32_t bank_size, float *mix_out,
                   void *stream);
+
+/* Registers the VeLO hypernetwork (same arguments as lopt_velo_mix) so that
+ * lopt_step / lopt_graph_step run it between phases 1 and 2 of a one-device
+ * step; hyper = NULL unregisters.  Element-sharded callers merge the stats
+ * first and call lopt_velo_mix themselves. */
+int lopt_set_velo(lopt_plan *plan, const float *hyper, float *lstm_state, const float *bank,
+                  const float *loss_feats, int32_t hidden, int32_t bank_size, float *mix_out);
 
 /* Known-answer test of the tcgen05 building blocks (device pointers):
  * D[128 x 32] f32 = A[128 x K] * B[32 x K]^T, K in {16,32,48,64}; flag bit 0:

@@ -5,6 +5,7 @@
 // tiles and phase-1/2 element chunks, and lays out one caller-owned device
 // workspace that holds the descriptor tables, the f64 partial sums and the
 // per-step scalars.  Steps then only launch kernels on the caller's stream.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -32,6 +33,21 @@ size_t prep_image_bytes();
 int64_t factor_strip_cols();
 int launch_velo_mix(const DevicePlan &P, const float *hyper, float *lstm_state, const float *bank,
                     const float *loss_feats, int H, int K, float *mix_out, cudaStream_t s);
+
+// First kernel of every step: publishes the step scalars (by value, so the
+// launch is stream-ordered and graph-capturable -- no pageable copy) and
+// clears the per-step status words, max |update|, abort flag and the
+// non-finite-gradient slot of the factor-sum block.
+__global__ void __launch_bounds__(256) begin_step_kernel(DevicePlan P, StepScalars h,
+                                                         int32_t write_scalars) {
+  if (write_scalars && threadIdx.x == 0 && blockIdx.x == 0) *P.step = h;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.count; j += gridDim.x * blockDim.x) {
+    P.status[j] = 0u;
+    P.maxabs[j] = 0.0f;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 4) P.abort_flag[threadIdx.x] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *P.grad_flag = 0.0;
+}
 }  // namespace lopt
 
 using namespace lopt;
@@ -91,6 +107,28 @@ struct lopt_plan {
   char *ws = nullptr;
   DevicePlan dp{};
   int launches_last_step = 0;
+  bool begun = false;        // lopt_set_step_args ran: the step's clears are done
+  // VeLO hypernetwork registered with lopt_set_velo: run between phases 1 and 2
+  bool velo = false;
+  const float *v_hyper = nullptr, *v_bank = nullptr, *v_loss = nullptr;
+  float *v_lstm = nullptr, *v_mix = nullptr;
+  int v_H = 0, v_K = 0;
+  // captured step (lopt_graph_step)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaGraphNode_t gbegin = nullptr;
+  void drop_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    gexec = nullptr;
+    graph = nullptr;
+    gbegin = nullptr;
+  }
+  ~lopt_plan() {
+    drop_graph();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+  }
 };
 
 static int check_cuda(cudaError_t e) {
@@ -427,9 +465,7 @@ int lopt_weights_ptr(lopt_plan *p, int32_t slot, float **dev_ptr) {
   return LOPT_OK;
 }
 
-int lopt_set_step_args(lopt_plan *p, const lopt_step_args *a, void *stream) {
-  if (!p || !p->ws || !a) return LOPT_ERR_INVALID;
-  if (!(a->weight_decay >= 0.0)) return LOPT_ERR_INVALID;
+static StepScalars make_scalars(const lopt_plan *p, const lopt_step_args *a) {
   StepScalars h{};
   for (int k = 0; k < kTimeFeatures; k++) h.tf[k] = a->time_features[k];
   h.lr_f32 = (float)a->lr;
@@ -437,23 +473,32 @@ int lopt_set_step_args(lopt_plan *p, const lopt_step_args *a, void *stream) {
   h.decay = (float)(1.0 - a->lr * a->weight_decay);             // optim.py:100
   h.apply_decay = a->weight_decay > 0.0 ? 1 : 0;                // optim.py:171
   h.t = a->t;
-  return check_cuda(cudaMemcpyAsync(p->dp.step, &h, sizeof(h), cudaMemcpyHostToDevice,
-                                    (cudaStream_t)stream));
+  return h;
+}
+
+static int begin_blocks(const lopt_plan *p) {
+  return (int)std::min<int64_t>(64, ((int64_t)p->tensors.size() + 255) / 256);
+}
+
+int lopt_set_step_args(lopt_plan *p, const lopt_step_args *a, void *stream) {
+  if (!p || !p->ws || !a) return LOPT_ERR_INVALID;
+  if (!(a->weight_decay >= 0.0)) return LOPT_ERR_INVALID;
+  const StepScalars h = make_scalars(p, a);
+  begin_step_kernel<<<begin_blocks(p), 256, 0, (cudaStream_t)stream>>>(p->dp, h, 1);
+  p->begun = true;
+  p->launches_last_step = 1;
+  return check_launch();
 }
 
 int lopt_factor_partials(lopt_plan *p, void *stream) {
   if (!p || !p->ws) return LOPT_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  int st;
-  if ((st = check_cuda(cudaMemsetAsync(p->ws + p->r_status.off, 0, p->r_status.bytes, s))))
-    return st;
-  if ((st = check_cuda(cudaMemsetAsync(p->ws + p->r_abort.off, 0, p->r_abort.bytes, s))))
-    return st;
-  if ((st = check_cuda(cudaMemsetAsync(p->ws + p->r_maxabs.off, 0, p->r_maxabs.bytes, s))))
-    return st;
-  if ((st = check_cuda(cudaMemsetAsync(p->dp.grad_flag, 0, sizeof(double), s)))) return st;
-  p->launches_last_step = 0;
-  if (p->cfg.state_advanced) return LOPT_OK;
+  if (!p->begun) {   // scalars from an earlier call: only the per-step clears
+    begin_step_kernel<<<begin_blocks(p), 256, 0, s>>>(p->dp, StepScalars{}, 0);
+    p->launches_last_step = 1;
+  }
+  p->begun = false;
+  if (p->cfg.state_advanced) return check_launch();
   launch_factor_partials(p->dp, s);
   launch_factor_reduce(p->dp, p->max_mn, s);
   p->launches_last_step += 2;
@@ -496,13 +541,102 @@ int lopt_apply(lopt_plan *p, void *stream) {
   return check_launch();
 }
 
+static int run_velo(lopt_plan *p, cudaStream_t s) {
+  const int st = launch_velo_mix(p->dp, p->v_hyper, p->v_lstm, p->v_bank, p->v_loss, p->v_H,
+                                 p->v_K, p->v_mix, s);
+  if (st == LOPT_OK) p->launches_last_step += 1;
+  return st;
+}
+
 int lopt_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
   int st;
   if (args && (st = lopt_set_step_args(p, args, stream))) return st;
   if ((st = lopt_factor_partials(p, stream))) return st;
   if ((st = lopt_factor_finalize(p, stream))) return st;
   if ((st = lopt_feature_stats(p, stream))) return st;
+  if (p->velo && (st = run_velo(p, (cudaStream_t)stream))) return st;
   return lopt_apply(p, stream);
+}
+
+int lopt_graph_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
+  if (!p || !p->ws || !args) return LOPT_ERR_INVALID;
+  if (!(args->weight_decay >= 0.0)) return LOPT_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  StepScalars h = make_scalars(p, args);
+  int st;
+  if (!p->gexec) {
+    // capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot be captured); the graph is launched on the caller's
+    if (!p->cap_stream &&
+        (st = check_cuda(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking))))
+      return st;
+    // the capture stream starts after the caller's prior work (descriptor
+    // uploads of bind/rebind) -- captured work itself is only enqueued later
+    if ((st = check_cuda(cudaStreamSynchronize(s)))) return st;
+    if ((st = check_cuda(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeRelaxed))))
+      return st;
+    int rc = lopt_set_step_args(p, args, p->cap_stream);
+    if (rc == LOPT_OK) rc = lopt_step(p, nullptr, p->cap_stream);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &g);
+    if (rc != LOPT_OK || ce != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      return rc != LOPT_OK ? rc : check_cuda(ce);
+    }
+    p->graph = g;
+    if ((st = check_cuda(cudaGraphInstantiate(&p->gexec, g, 0)))) {
+      p->drop_graph();
+      return st;
+    }
+    // the step-scalar kernel is the graph's only root
+    size_t nroot = 1;
+    cudaGraphNode_t root = nullptr;
+    if ((st = check_cuda(cudaGraphGetRootNodes(g, &root, &nroot))) || nroot != 1) {
+      p->drop_graph();
+      return st ? st : LOPT_ERR_CUDA;
+    }
+    p->gbegin = root;
+  }
+  cudaKernelNodeParams kp{};
+  if ((st = check_cuda(cudaGraphKernelNodeGetParams(p->gbegin, &kp)))) return st;
+  int32_t one = 1;
+  void *kargs[3] = {&p->dp, &h, &one};
+  kp.kernelParams = kargs;
+  kp.extra = nullptr;
+  if ((st = check_cuda(cudaGraphExecKernelNodeSetParams(p->gexec, p->gbegin, &kp)))) return st;
+  return check_cuda(cudaGraphLaunch(p->gexec, s));
+}
+
+int lopt_graph_reset(lopt_plan *p) {
+  if (!p) return LOPT_ERR_INVALID;
+  p->drop_graph();
+  return LOPT_OK;
+}
+
+int lopt_set_velo(lopt_plan *p, const float *hyper, float *lstm_state, const float *bank,
+                  const float *loss_feats, int32_t hidden, int32_t bank_size, float *mix_out) {
+  if (!p || !p->ws) return LOPT_ERR_INVALID;
+  p->drop_graph();   // the captured step changes
+  if (!hyper) {      // unregister
+    p->velo = false;
+    return LOPT_OK;
+  }
+  if (!lstm_state || !bank || !loss_feats || hidden < 1 || hidden > 64 || bank_size < 1 ||
+      bank_size > 16 || p->cfg.feature_set != LOPT_VELO_MLP)
+    return LOPT_ERR_INVALID;
+  if (p->cfg.num_weight_sets != (int32_t)p->tensors.size()) return LOPT_ERR_INVALID;
+  for (size_t j = 0; j < p->tensors.size(); j++)
+    if (p->tensors[j].weight_slot != (int32_t)j) return LOPT_ERR_INVALID;
+  p->velo = true;
+  p->v_hyper = hyper;
+  p->v_lstm = lstm_state;
+  p->v_bank = bank;
+  p->v_loss = loss_feats;
+  p->v_H = hidden;
+  p->v_K = bank_size;
+  p->v_mix = mix_out;
+  return LOPT_OK;
 }
 
 int lopt_factor_sums_ptr(lopt_plan *p, double **ptr, int64_t *count) {
@@ -567,6 +701,7 @@ int lopt_set_peers(lopt_plan *p, int32_t count, const int64_t *deltas) {
   if (count > 0 && p->cfg.mode != LOPT_MODE_FAST) return LOPT_ERR_UNSUPPORTED;
   p->dp.n_peers = count;
   for (int k = 0; k < LOPT_MAX_PEERS; k++) p->dp.peer_delta[k] = k < count ? deltas[k] : 0;
+  p->drop_graph();   // the plan is captured by value
   return LOPT_OK;
 }
 

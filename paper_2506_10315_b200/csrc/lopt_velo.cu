@@ -25,6 +25,10 @@ __global__ void __launch_bounds__(256) velo_mix_kernel(DevicePlan P, const float
                                                        float *lstm_state, const float *bank,
                                                        const float *loss_feats, int H, int K,
                                                        float *mix_out) {
+  // a non-finite gradient anywhere in the step (the flag is set by
+  // factor_finalize from the all-reduced factor block) changes nothing --
+  // optim.py:160-165 -- so the LSTM state must not advance either
+  if (*P.abort_flag != 0) return;
   const int j = blockIdx.x;
   const TensorDesc T = P.tensors[j];
   __shared__ float x[kVeloIn];

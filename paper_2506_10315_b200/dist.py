@@ -302,8 +302,16 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
                 view.copy_(p.grad.reshape(-1))
                 p.grad = view.view(p.shape)
         b = h["bucket_of"][j]
+        if b in h["works"]:
+            # a second backward into a bucket whose reduce-scatter is already
+            # in flight: it would race with the collective writing the same
+            # arena segment and add into an already-reduced portion
+            raise RuntimeError(
+                "gradient accumulation across backward passes is not supported with "
+                "overlap_grad_reduce(): call step() (or zero_grad()) after every backward, "
+                "or accumulate with overlapped reduction turned off")
         h["ready"][b] += 1
-        if h["ready"][b] == len(self.buckets[b][2]) and b not in h["works"]:
+        if h["ready"][b] == len(self.buckets[b][2]):
             h["works"][b] = self._bucket_rs(b, h["average"], async_op=True)
 
     def _finish_grad_reduce(self):
@@ -321,6 +329,15 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
         """With a gradient arena the views are kept and the arena is zeroed in
         place (backward must accumulate into the arena)."""
         if getattr(self, "_flat_grad", None) is not None:
+            h = self._rs_hooks
+            if h is not None and h["works"]:
+                # reductions of a backward that is being discarded: let them
+                # finish before the arena they write is cleared
+                for w in h["works"].values():
+                    if w is not None:
+                        w.wait()
+                h["works"] = {}
+                h["ready"] = [0] * len(self.buckets)
             self._flat_grad.zero_()
             return
         super().zero_grad(set_to_none=set_to_none)
@@ -426,6 +443,27 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
                 dist.all_gather(chunks, local.cpu(), group=self.pg)
                 seg.copy_(torch.cat(chunks).to(seg.device))
 
+    def load_state_dict(self, state_dict):
+        """LearnedOptimizer.load_state_dict, then a layout check: every tensor's
+        saved element range must be the one this rank steps under the current
+        world size (a state saved by another rank, or under another world
+        size, would otherwise update the wrong slice)."""
+        from .optim import OptimError
+
+        super().load_state_dict(state_dict)
+        for j, p in enumerate(self.param_groups[0]["params"]):
+            st = self.state[p]
+            got = tuple(int(x) for x in st.get("range", (-1, -1)))
+            if got != tuple(self.ranges[j]):
+                raise OptimError(f"tensor {j}: saved element range {got} is not this rank's "
+                                 f"range {tuple(self.ranges[j])} (rank {self.rank} of "
+                                 f"{self.world}); load the state saved by this rank")
+            n = self.ranges[j][1] - self.ranges[j][0]
+            if "quad" in st and st["quad"].shape[0] != max(n, 1):
+                raise OptimError(f"tensor {j}: state holds {st['quad'].shape[0]} elements, "
+                                 f"the range has {n}")
+            st["range"] = tuple(self.ranges[j])
+
     def local_state_bytes(self) -> int:
         return sum(int(st["quad"].numel()) * 4 for st in self.state.values() if "quad" in st)
 
@@ -449,8 +487,20 @@ def _sharded_velo_cls():
             if closure is not None:
                 with torch.enable_grad():
                     loss = closure()
-            self._set_loss(loss)
+            if loss is None:
+                self._set_loss(None)   # raises: VeLO needs the loss
+            # the hypernetwork's loss features must be the same on every rank
+            # (each rank mixes the MLP for its slices of the same tensors):
+            # the data-parallel batch loss, i.e. the mean of the ranks' losses
+            self._set_loss(self.global_loss(loss))
             return super().step(loss=loss)
+
+        def global_loss(self, loss) -> float:
+            """Mean of `loss` over the ranks of the process group."""
+            dev = self.flat.device if self._nccl() else "cpu"
+            t = torch.tensor([float(loss)], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, group=self.pg)
+            return float(t.item()) / self.world
 
     return ShardedVeLO
 

@@ -39,8 +39,9 @@ class UpdateOverflowError(EngineError):
 
 
 def _stream_handle(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    return torch.cuda.current_stream().cuda_stream
 
 
 @dataclass
@@ -128,6 +129,10 @@ class StepPlan:
         self._packed = []
         for slot, w in enumerate(weights_list):
             self.set_weights(slot, w)
+        self._step_args = _lib.lopt_step_args()
+        self.graph_steps = 0
+        self._tf_t = None
+        self._velo_key = None
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -158,18 +163,8 @@ class StepPlan:
                                               _stream_handle()), "rebind_tensors")
 
     def set_step(self, lr: float, weight_decay: float, t: int):
-        args = _lib.lopt_step_args()
-        args.lr = float(lr)
-        args.weight_decay = float(weight_decay)
-        # tanh(t/x) for all 11 horizons: the small_fc_lopt columns
-        # (features.py:125-130) and the VeLO hypernetwork inputs; the
-        # VELO_MLP per-element kernels ignore them
-        tf = time_features(t, small_fc_lopt_spec())
-        for k in range(11):
-            args.time_features[k] = float(tf[k])
-        args.t = int(t)
-        _lib.check(self.L.lopt_set_step_args(self.h, ctypes.byref(args), _stream_handle()),
-                   "set_step_args")
+        _lib.check(self.L.lopt_set_step_args(self.h, ctypes.byref(self._args(lr, weight_decay, t)),
+                                             _stream_handle()), "set_step_args")
 
     # -- phases ----------------------------------------------------------
     def factor_partials(self):
@@ -184,9 +179,48 @@ class StepPlan:
     def apply(self):
         _lib.check(self.L.lopt_apply(self.h, _stream_handle()), "apply")
 
+    def _args(self, lr: float, weight_decay: float, t: int):
+        args = self._step_args
+        args.lr = float(lr)
+        args.weight_decay = float(weight_decay)
+        # tanh(t/x) for all 11 horizons: the small_fc_lopt columns
+        # (features.py:125-130) and the VeLO hypernetwork inputs; the
+        # VELO_MLP per-element kernels ignore them
+        if t != self._tf_t:
+            tf = time_features(t, small_fc_lopt_spec())
+            for k in range(11):
+                args.time_features[k] = float(tf[k])
+            self._tf_t = t
+        args.t = int(t)
+        return args
+
     def step(self, lr: float, weight_decay: float, t: int):
-        self.set_step(lr, weight_decay, t)
-        _lib.check(self.L.lopt_step(self.h, None, _stream_handle()), "step")
+        _lib.check(self.L.lopt_step(self.h, ctypes.byref(self._args(lr, weight_decay, t)),
+                                    _stream_handle()), "step")
+
+    def graph_step(self, lr: float, weight_decay: float, t: int):
+        """step() replayed from the plan's captured CUDA graph (one launch)."""
+        _lib.check(self.L.lopt_graph_step(self.h, ctypes.byref(self._args(lr, weight_decay, t)),
+                                          _stream_handle()), "graph_step")
+        self.graph_steps += 1
+
+    def gexec_ready(self) -> bool:
+        """True once a step ran from the captured graph."""
+        return self.graph_steps > 0
+
+    def set_velo(self, hyper, lstm, bank, loss, hidden, bank_size, mix=None):
+        """Register the VeLO hypernetwork (device tensors) so step() and
+        graph_step() run it between phases 1 and 2; hyper=None unregisters."""
+        if hyper is None:
+            _lib.check(self.L.lopt_set_velo(self.h, None, None, None, None, 0, 0, None))
+            self._velo_key = None
+            return
+        _lib.check(self.L.lopt_set_velo(self.h, hyper.data_ptr(), lstm.data_ptr(),
+                                        bank.data_ptr(), loss.data_ptr(), int(hidden),
+                                        int(bank_size), mix.data_ptr() if mix is not None else None),
+                   "set_velo")
+        self._velo_key = (hyper.data_ptr(), lstm.data_ptr(), bank.data_ptr(), loss.data_ptr(),
+                          mix.data_ptr() if mix is not None else None)
 
     def set_peers(self, deltas):
         """Fused parameter all-gather: the apply pass also stores every updated

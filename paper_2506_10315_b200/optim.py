@@ -84,7 +84,9 @@ class LearnedOptimizer(torch.optim.Optimizer):
         weights: LoptWeights; default random_weights(d_feat, seed=weights_seed).
         schedule: optional reference ScheduleConfig; when given it overrides
             group lr with schedule_lr(schedule, T) at the pre-increment T.
-        mode: "fast" (tensor-core MLP, fp32 tolerance) or "strict" (bitwise).
+        mode: "fast" (the default: tensor-core MLP within the fp32 tolerance
+            of the reference, states bitwise) or "strict" (every output
+            bitwise the reference's; about 4x slower).
         check_errors: synchronize after each step to raise OptimError /
             UpdateOverflowError like the reference; False keeps steps async
             (call `check()` to surface errors later).
@@ -93,7 +95,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
     def __init__(self, params, lr: float = 1.0, weight_decay: float = 0.0, *,
                  feature_set: str = "small_fc_lopt", weights: LoptWeights | None = None,
                  weights_seed: int = 0, schedule: ScheduleConfig | None = None,
-                 mode: str = "strict", check_errors: bool = True):
+                 mode: str = "fast", check_errors: bool = True):
         if lr < 0:
             raise ValueError(f"invalid learning rate {lr}")
         if weight_decay < 0:
@@ -149,22 +151,33 @@ class LearnedOptimizer(torch.optim.Optimizer):
         return self.lopt_weights, [0] * len(params)
 
     def _plan_for_group(self, gi, params):
-        key = tuple(id(p) for p in params)
+        """The group's StepPlan.  Steady state costs one pointer comparison per
+        tensor: the plan (and its captured graph) is reused while the same
+        parameters carry gradients at the same addresses; moved tensors are
+        re-pointed (lopt_rebind_tensors), a different parameter set builds a
+        new plan."""
+        key = tuple(map(id, params))
+        cached = self._plans.get(gi)
+        if cached is not None and cached[0] == key:
+            _, plan, ptrs = cached
+            try:
+                now = [(p.data_ptr(), p.grad.data_ptr()) for p in params]
+            except AttributeError:
+                now = None
+            if now == ptrs:
+                return plan
         weights, slots_idx = self._weights_for_group(gi, params)
         slots = [self._slot(p, k) for p, k in zip(params, slots_idx)]
-        cached = self._plans.get(gi)
+        ptrs = [(s.theta.data_ptr(), s.grad.data_ptr()) for s in slots]
         if cached is None or cached[0] != key:
             plan = StepPlan(slots, self.spec, weights, mode=self.mode)
             if getattr(self, "_peer_deltas", None):
                 plan.set_peers(self._peer_deltas)
-            self._plans[gi] = (key, plan, [(s.theta.data_ptr(), s.grad.data_ptr()) for s in slots])
         else:
-            _, plan, ptrs = cached
-            now = [(s.theta.data_ptr(), s.grad.data_ptr()) for s in slots]
-            if now != ptrs:
-                plan.rebind(slots)
-                self._plans[gi] = (key, plan, now)
-        return self._plans[gi][1]
+            plan = cached[1]
+            plan.rebind(slots)
+        self._plans[gi] = (key, plan, ptrs)
+        return plan
 
     # -- step --------------------------------------------------------------
     @torch.no_grad()
@@ -190,10 +203,6 @@ class LearnedOptimizer(torch.optim.Optimizer):
         if self.check_errors:
             self.check()   # raises before the counter moves, like opt_step
         self.T += 1
-        for group in self.param_groups:
-            for p in group["params"]:
-                if p in self.state and "quad" in self.state[p]:
-                    self.state[p]["step"] = self.T
         return loss
 
     # Hook run after the feature statistics are final and before phase 2
@@ -214,9 +223,22 @@ class LearnedOptimizer(torch.optim.Optimizer):
         b.record()
         self.phase_events.append((name, a, b))
 
+    # False: every step launches its kernels one by one (lopt_step) instead of
+    # replaying the plan's captured CUDA graph (lopt_graph_step)
+    use_graph = True
+
+    def _single_call(self, gi, plan, params) -> bool:
+        """True if the whole step of this plan is one C call (VeLO registers
+        its hypernetwork on the plan here)."""
+        return self._after_stats is None
+
     def _run_plan(self, plan, lr, weight_decay, t, gi, params):
-        if self.phase_events is None and self._after_stats is None:
-            plan.step(lr, weight_decay, t)   # one C call: all phases
+        if self.phase_events is None and self._single_call(gi, plan, params):
+            # one C call: all phases (from the captured graph after the first)
+            if self.use_graph:
+                plan.graph_step(lr, weight_decay, t)
+            else:
+                plan.step(lr, weight_decay, t)
             return
         plan.set_step(lr, weight_decay, t)
         self._timed("factors", lambda: (plan.factor_partials(), plan.factor_finalize()))
@@ -404,9 +426,6 @@ class LearnedOptimizer(torch.optim.Optimizer):
         if self.check_errors:
             self.check()
         self.T += 1
-        for p in params:
-            if "quad" in self.state[p]:
-                self.state[p]["step"] = self.T
         return None
 
     def check(self):
@@ -438,6 +457,9 @@ class LearnedOptimizer(torch.optim.Optimizer):
 
     # -- checkpointing -------------------------------------------------------
     def state_dict(self):
+        for st in self.state.values():   # the per-tensor step counter, kept lazily
+            if "quad" in st:
+                st["step"] = self.T
         sd = super().state_dict()
         sd["lopt"] = {"T": self.T, "feature_set": self.spec.id.value, "mode": self.mode,
                       "weights": [(w.copy(), b.copy()) for w, b in self.lopt_weights.layers]}

@@ -77,8 +77,9 @@ class _VeLOMixin:
         return [self.hypernet.bank[0]] * len(params), list(range(len(params)))
 
     def _lstm_state(self, gi, params):
-        st = self._lstm.get(gi)
-        if st is None or st.shape[0] != len(params):
+        key = tuple(id(p) for p in params)
+        st, old_key = self._lstm.get(gi, (None, None))
+        if st is None or old_key != key:
             # one contiguous [tensors x 2H] block per group for the kernel;
             # rows start from the tensors' current LSTM state (a resumed or
             # regrouped optimizer continues where it was)
@@ -89,7 +90,9 @@ class _VeLOMixin:
                 if prev is not None:
                     st[j].copy_(prev.to(device=dev, dtype=torch.float32).reshape(-1))
                 self.state[p]["lstm"] = st[j]
-            self._lstm[gi] = st
+            # keyed by the parameters' identities: if the set of tensors with
+            # gradients changes, each tensor keeps its own row
+            self._lstm[gi] = (st, key)
         return st
 
     def state_dict(self):
@@ -107,6 +110,9 @@ class _VeLOMixin:
         if loss is None:
             raise OptimError("VeLO needs the loss: call optimizer.step(loss) (PAPER.md:600)")
         lv = math.log(max(float(loss), 1e-8))
+        # kept so that a step that changes nothing (non-finite gradient,
+        # optim.py:160-165) also leaves the loss EMA where it was (check())
+        self._loss_ema_prev = self._loss_ema
         self._loss_ema = lv if self._loss_ema is None else 0.9 * self._loss_ema + 0.1 * lv
         # stream-ordered upload from a small ring of pinned buffers (a pageable
         # copy would stall the host on every step)
@@ -121,6 +127,29 @@ class _VeLOMixin:
         buf[0], buf[1] = lv, self._loss_ema
         self._loss_dev.copy_(buf, non_blocking=True)
         ev.record()
+
+    def check(self):
+        """LearnedOptimizer.check; an aborted step (OptimError: non-finite
+        gradient) also rolls the loss EMA back -- on the device the
+        hypernetwork kernel skipped the LSTM update (lopt_velo.cu)."""
+        try:
+            super().check()
+        except OptimError:
+            if hasattr(self, "_loss_ema_prev"):
+                self._loss_ema = self._loss_ema_prev
+            raise
+
+    def _single_call(self, gi, plan, params) -> bool:
+        """One-device step: the hypernetwork is registered on the plan and
+        runs inside lopt_step / the captured graph."""
+        st = self._lstm_state(gi, params)
+        mix = getattr(self, "_mix_out", None)
+        key = (self._hyper_dev.data_ptr(), st.data_ptr(), self._bank_dev.data_ptr(),
+               self._loss_dev.data_ptr(), mix.data_ptr() if mix is not None else None)
+        if plan._velo_key != key:
+            plan.set_velo(self._hyper_dev, st, self._bank_dev, self._loss_dev, self.hypernet.H,
+                          self.hypernet.K, mix)
+        return True
 
     def _after_stats(self, gi, plan, params):
         st = self._lstm_state(gi, params)

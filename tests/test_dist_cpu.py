@@ -337,3 +337,75 @@ def test_reduce_scatter_overlapped_with_backward_gloo_world2():
         assert nb > 1 and launched == nb
         for (off, (lo, hi), g), m in zip(out, mean):
             np.testing.assert_allclose(g[lo:hi], m[lo:hi], rtol=1e-6, atol=1e-9)
+
+
+def _guard_worker(rank, world, port, q):
+    """Accumulating a second backward into buckets whose reduce-scatter was
+    already launched must raise (it would race with the collective and
+    double-count); a state_dict saved by the other rank must not load."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    try:
+        from paper_2506_10315_b200.dist import ShardedLearnedOptimizer
+        from paper_2506_10315_b200.optim import OptimError
+
+        torch.manual_seed(0)
+        model = torch.nn.Sequential(torch.nn.Linear(16, 32), torch.nn.ReLU(),
+                                    torch.nn.Linear(32, 8))
+        opt = ShardedLearnedOptimizer(model.parameters(), bucket_elems=200)
+        opt.overlap_grad_reduce(average=True)
+        x, y = torch.randn(4, 16), torch.randn(4, 8)
+        torch.nn.functional.mse_loss(model(x), y).backward()
+        try:
+            torch.nn.functional.mse_loss(model(x), y).backward()
+            out["accum"] = "no error"
+        except RuntimeError as e:
+            out["accum"] = "raised" if "accumulation" in str(e) else str(e)
+        # zero_grad waits for / clears the outstanding bucket reductions
+        opt.zero_grad()
+        torch.nn.functional.mse_loss(model(x), y).backward()
+        out["after_zero"] = len(opt._rs_hooks["works"]) == len(opt.buckets)
+        # checkpoint layout check
+        mine = opt.state_dict()
+        objs = [None] * world
+        dist.all_gather_object(objs, mine)
+        other = objs[1 - rank]
+        try:
+            opt.load_state_dict(other)
+            out["foreign"] = "loaded"
+        except OptimError:
+            out["foreign"] = "raised"
+        opt.load_state_dict(objs[rank])
+        out["own"] = "loaded"
+        q.put((rank, out))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlap_guard_and_sharded_state_layout_check_gloo_world2():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_guard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=30)
+    for rank, out in res:
+        assert isinstance(out, dict), out
+        assert out == {"accum": "raised", "after_zero": True, "foreign": "raised",
+                       "own": "loaded"}, out

@@ -276,7 +276,9 @@ def _velo_worker(rank, world, port, mode, strategy, q):
         for k, gs in enumerate(grads):
             for p, g in zip(params, gs):
                 p.grad = torch.from_numpy(g).cuda()
-            opt.step(loss=2.5 - 0.1 * k)
+            # rank-local losses differ (each rank sees its own batch); the
+            # hypernetwork must see their mean on every rank
+            opt.step(loss=2.5 - 0.1 * k + (0.4 if rank == 0 else -0.4))
         torch.cuda.synchronize()
         q.put((rank, [p.detach().cpu().numpy().copy() for p in params]))
         dist.destroy_process_group()
@@ -287,9 +289,10 @@ def _velo_worker(rank, world, port, mode, strategy, q):
 @pytest.mark.parametrize("mode,strategy", [("strict", "range"), ("strict", "owner"),
                                            ("fast", "range")])
 def test_sharded_velo_equals_single_gpu(mode, strategy):
-    """The full VeLO optimizer sharded over two ranks: every rank runs the
-    per-tensor LSTM on the merged statistics, so all ranks mix the same MLPs
-    and the result equals VeLO_CUDA on one GPU (bitwise in strict mode)."""
+    """The full VeLO optimizer sharded over two ranks with DIFFERENT local
+    losses: every rank runs the per-tensor LSTM on the merged statistics and
+    the mean loss, so all ranks mix the same MLPs and the result equals
+    VeLO_CUDA on one GPU stepped with the mean loss (bitwise in strict mode)."""
     import torch
     import torch.multiprocessing as mp
 
@@ -322,3 +325,93 @@ def test_sharded_velo_equals_single_gpu(mode, strategy):
             else:
                 err = np.abs(a.astype(np.float64) - b) / (1 + np.abs(b))
                 assert err.max() <= 1e-6, err.max()
+
+
+def _nccl_worker(port, q):
+    """World size 1 over NCCL: every collective branch of dist.py runs on the
+    real backend (all_reduce of the factor / stats / flag blocks,
+    all_gather_into_tensor of the parameter arena, reduce_scatter_tensor of
+    the gradient buckets from the backward hooks, the VeLO loss mean)."""
+    import sys
+    import traceback
+
+    sys.path.insert(0, ROOT)
+    try:
+        import torch
+        import torch.distributed as dist
+
+        import paper_2506_10315_b200 as P
+        from paper_2506_10315_b200.dist import ShardedLearnedOptimizer, ShardedVeLO
+
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+        assert dist.get_backend() == "nccl"
+        init, grads = _init()
+        results = {}
+        for name in ("range", "owner", "bucketed", "velo", "single", "single_velo"):
+            ps = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+            if name == "single":
+                opt = P.LearnedOptimizer(ps, mode="fast", weight_decay=0.01)
+            elif name == "single_velo":
+                opt = P.VeLO_CUDA(ps, mode="fast", weight_decay=0.01)
+            elif name == "velo":
+                opt = ShardedVeLO(ps, mode="fast", weight_decay=0.01)
+            elif name == "bucketed":
+                opt = ShardedLearnedOptimizer(ps, mode="fast", weight_decay=0.01,
+                                              bucket_elems=20000)
+                opt.overlap_grad_reduce(average=True)
+            else:
+                opt = ShardedLearnedOptimizer(ps, mode="fast", weight_decay=0.01,
+                                              strategy=name)
+            for k, gs in enumerate(grads):
+                if name == "bucketed":
+                    # gradients produced by a backward pass: the hooks launch
+                    # each bucket's NCCL reduce-scatter as it completes
+                    opt.zero_grad()
+                    loss = sum((p * torch.from_numpy(g).cuda()).sum() for p, g in zip(ps, gs))
+                    loss.backward()
+                else:
+                    for p, g in zip(ps, gs):
+                        p.grad = torch.from_numpy(g).cuda()
+                if name in ("velo", "single_velo"):
+                    opt.step(loss=2.0 - 0.1 * k)
+                else:
+                    opt.step()
+            torch.cuda.synchronize()
+            results[name] = [p.detach().cpu().numpy().copy() for p in ps]
+        # explicit reduce-scatter entry point on the NCCL backend as well
+        ps = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+        opt = ShardedLearnedOptimizer(ps, mode="fast")
+        fg = opt.flat_grads()
+        fg.fill_(2.0)
+        sl = opt.reduce_scatter_grads(average=True)
+        results["rs_ok"] = bool(torch.all(sl == 2.0).item())
+        q.put(results)
+        dist.destroy_process_group()
+    except Exception:
+        q.put(traceback.format_exc())
+
+
+def test_nccl_world_size_one_runs_every_collective():
+    """The NCCL code paths of dist.py (never executed by the gloo tests) on
+    the box's GPU with a one-rank NCCL group: every sharded variant equals the
+    single-GPU optimizer bitwise (one rank owns everything; the collectives
+    are identities that must not corrupt anything)."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_nccl_worker, args=(_free_port(), q))
+    pr.start()
+    res = q.get(timeout=600)
+    pr.join(timeout=60)
+    assert not isinstance(res, str), res
+    assert res["rs_ok"]
+    for name in ("range", "owner", "bucketed"):
+        for a, b in zip(res[name], res["single"]):
+            assert a.tobytes() == b.tobytes(), name
+    for a, b in zip(res["velo"], res["single_velo"]):
+        assert a.tobytes() == b.tobytes()

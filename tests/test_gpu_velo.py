@@ -52,7 +52,7 @@ def test_velo_step_matches_oracle_with_mixed_mlps(oracle, mode):
         mixed, alphas, lstm = V.velo_mix(hn.hyper, lstm, bank, sumsq, counts, step + 1, lf,
                                          H=hn.H, K=hn.K)
         np.testing.assert_allclose(opt._mix_out.cpu().numpy(), alphas, rtol=1e-5, atol=1e-6)
-        gpu_lstm = opt._lstm[0].cpu().numpy()
+        gpu_lstm = opt._lstm[0][0].cpu().numpy()
         np.testing.assert_allclose(gpu_lstm, lstm, rtol=1e-5, atol=1e-6)
         lstm = gpu_lstm.copy()   # continue from the device state (tolerance, not drift)
         ws = [P.weights.unpack(m, 29) for m in mixed]
@@ -173,3 +173,47 @@ def test_velo_state_dict_resume_is_bitwise(mode):
     torch.cuda.synchronize()
     for p, q in zip(a, b):
         assert p.detach().cpu().numpy().tobytes() == q.detach().cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_velo_nonfinite_gradient_changes_nothing_then_recovers(mode):
+    """optim.py:160-165 for the whole VeLO step: a non-finite gradient raises
+    OptimError and changes nothing -- parameters, accumulators, factors, the
+    per-tensor LSTM state and the loss EMA -- and the next finite step equals
+    the step of an optimizer that never saw the bad one (bitwise)."""
+    import torch
+
+    import paper_2506_10315_b200 as P
+
+    rng, init, params, hn, opt = _setup(P, mode)
+    ref = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    opt_ref = P.VeLO_CUDA(ref, weight_decay=0.01, hypernet=hn, mode=mode)
+    g1 = [np.asarray(rng.standard_normal(p.shape) * 1e-2, F32) for p in init]
+    g2 = [np.asarray(rng.standard_normal(p.shape) * 1e-2, F32) for p in init]
+    for o, ps in ((opt, params), (opt_ref, ref)):
+        for p, g in zip(ps, g1):
+            p.grad = torch.from_numpy(g).cuda()
+        o.step(loss=2.0)
+    lstm0 = opt._lstm[0][0].clone()
+    ema0 = opt._loss_ema
+    theta0 = [p.detach().clone() for p in params]
+    quad0 = [opt.state[p]["quad"].clone() for p in params]
+    bad = [torch.from_numpy(g).cuda() for g in g2]
+    bad[2].view(-1)[17] = float("inf")
+    for p, g in zip(params, bad):
+        p.grad = g
+    with pytest.raises(P.OptimError):
+        opt.step(loss=1.5)
+    assert torch.equal(opt._lstm[0][0], lstm0)
+    assert opt._loss_ema == ema0
+    for p, t0, q0 in zip(params, theta0, quad0):
+        assert torch.equal(p.detach(), t0)
+        assert torch.equal(opt.state[p]["quad"], q0)
+    for o, ps in ((opt, params), (opt_ref, ref)):
+        for p, g in zip(ps, g2):
+            p.grad = torch.from_numpy(g).cuda()
+        o.step(loss=1.5)
+    for a, b in zip(params, ref):
+        assert torch.isfinite(a).all()
+        assert torch.equal(a.detach(), b.detach())
+    assert torch.equal(opt._lstm[0][0], opt_ref._lstm[0][0])
