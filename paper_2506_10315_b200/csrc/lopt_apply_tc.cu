@@ -238,7 +238,8 @@ struct Producer {
     }
   }
 
-  __device__ __forceinline__ void stage(Stage &st, uint64_t *full, int img, int img_par) {
+  __device__ __forceinline__ void stage(Stage &st, uint64_t *full, int img, int img_par,
+                                        int tail_tiles = kWGsC) {
     TileMeta mt;
     mt.j = j;
     mt.b0 = b0;
@@ -250,7 +251,7 @@ struct Producer {
     mt.v0 = v0;
     mt.v1 = v1;
     const bool fast = aligned && ((el0 + v0) & 3) == 0 && ((v1 - v0) & 3) == 0;
-    mt.flags = (rb ? kFlagRowblock : 0) | (fast ? 0 : kFlagSlow) | (left <= kWGsC ? kFlagTail : 0);
+    mt.flags = (rb ? kFlagRowblock : 0) | (fast ? 0 : kFlagSlow) | (left <= tail_tiles ? kFlagTail : 0);
     mt.img = img;
     mt.img_par = img_par;
     mt.pad0[0] = mt.pad0[1] = mt.pad0[2] = 0;
@@ -745,6 +746,331 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
   if (warp == 0) tc::tmem_dealloc(tbase, kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// Unified-warpgroup pipeline (the default): every math warpgroup carries its
+// own tiles through all stages -- features, layer-1 MMAs, layer-1 epilogue,
+// layer-2 MMAs, layer 3 + update -- in its own TMEM slot, issuing its MMAs
+// from an elected lane of its first warp.  kUniWGs warpgroups interleave, so
+// while one waits for its MMAs the others compute; there are no hand-offs
+// between roles (the per-tile waits are the warpgroup's own TMA data and its
+// two MMA commits), which removes most of the barrier polling and per-role
+// bookkeeping of the role-specialized pipeline above, and each thread keeps
+// its element's values in registers from load to store.
+constexpr int kUniWGs = 4;
+constexpr int kUniRing = 16;
+constexpr int kUniProducers = 2;
+constexpr int kUniThreads = kUniWGs * 128 + kUniProducers * 32;
+constexpr int kUniWarpProducer = kUniWGs * 4;
+constexpr uint32_t kUniOneCol = kSlotCols * kUniWGs;
+static_assert(kUniOneCol + 8 <= kTmemCols, "TMEM budget");
+
+struct __align__(1024) UniSmem {
+  PrepImage img[kImgs];
+  Stage stage[kUniRing];
+  uint64_t full[kUniRing];       // producer -> WG: tile staged (TMA complete_tx)
+  uint64_t data_free[kUniRing];  // WG -> producer (128 arrivals)
+  uint64_t acc[kUniWGs];         // MMA commits of the WG (two phases per tile)
+  uint64_t img_full[kImgs];      // producer -> WGs: operand image loaded
+  int32_t done[kUniWGs][4];      // WG warps: last tile finished (image-buffer reuse)
+  uint32_t tmem_base;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(kUniThreads, 1) apply_uni_kernel(DevicePlan P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  UniSmem &S = *reinterpret_cast<UniSmem *>(smem_raw);
+  const int tid = threadIdx.x;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int row = tid & 127;
+  if (warp == 0) {
+    tc::tmem_alloc(&S.tmem_base, kTmemCols);
+    tc::tmem_relinquish();
+  }
+  if (tid == 0) {
+    for (int r = 0; r < kUniRing; r++) {
+      tc::mbar_init(&S.full[r], 1);
+      tc::mbar_init(&S.data_free[r], 128);
+    }
+    for (int b = 0; b < kImgs; b++) tc::mbar_init(&S.img_full[b], 1);
+    for (int w = 0; w < kUniWGs; w++) {
+      tc::mbar_init(&S.acc[w], 1);
+      for (int q = 0; q < 4; q++) S.done[w][q] = -1;
+    }
+    tc::mbar_fence_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tbase = S.tmem_base;
+  const uint32_t lane_addr = (uint32_t)((warp & 3) * 32) << 16;
+  if (warp < 4) {
+    // the constant slice that selects the layer-2 bias: fp16 {1, 1, 0, ...}
+    const uint32_t one[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    tc::tmem_st8(tbase + lane_addr + kUniOneCol, one);
+    tc::tmem_st_wait();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const bool aborted = *P.abort_flag != 0;
+  const int32_t tb = (int32_t)(P.n_tiles * blockIdx.x / gridDim.x);
+  const int32_t te = (int32_t)(P.n_tiles * (blockIdx.x + 1) / gridDim.x);
+  const int32_t nt = aborted ? 0 : te - tb;
+
+  if (warp >= kUniWarpProducer) {
+    // -------------------------------------------------------------- producers
+    const int p = warp - kUniWarpProducer;
+    if (tc::elect_one() && nt > 0) {
+      Producer pr;
+      pr.seek(P, tb);
+      int k = -1, img = 0, cur_j = -1;
+      uint32_t par_bits = 0;
+      int32_t first[kImgs] = {0, 0, 0, 0};
+      Cursor<kUniRing> rc;
+      for (int32_t i = 0; i < nt; i++) {
+        if (pr.j != cur_j) {
+          cur_j = pr.j;
+          k++;
+          img = k & (kImgs - 1);
+          const int32_t pf = first[img];
+          const int32_t nf = first[(k + 1) & (kImgs - 1)];
+          first[img] = i;
+          if (k >= kImgs) par_bits ^= 1u << img;
+          if (i % kUniProducers == p) {
+            if (k >= kImgs) {
+              // tensor k - kImgs used tiles [pf, nf - 1]: every warp of every
+              // WG must be past its last tile in that range
+              const int32_t last = nf - 1;
+              for (int w = 0; w < kUniWGs; w++) {
+                const int32_t need = last - (((last - w) % kUniWGs) + kUniWGs) % kUniWGs;
+                if (need < pf) continue;
+                for (int q = 0; q < 4; q++) {
+                  int32_t d;
+                  while (true) {
+                    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];\n"
+                                 : "=r"(d)
+                                 : "r"(tc::smem_u32(&S.done[w][q]))
+                                 : "memory");
+                    if (d >= need) break;
+                    __nanosleep(32);
+                  }
+                }
+              }
+            }
+            mbar_arrive_tx(&S.img_full[img], (uint32_t)sizeof(PrepImage));
+            bulk_g2s(&S.img[img], reinterpret_cast<const PrepImage *>(P.prep) + pr.j,
+                     (uint32_t)sizeof(PrepImage), &S.img_full[img]);
+          }
+        }
+        if (i % kUniProducers == p) {
+          if (rc.wrapped) tc::mbar_wait(&S.data_free[rc.i], rc.phase ^ 1u);
+          pr.stage(S.stage[rc.i], &S.full[rc.i], img, (int)((par_bits >> img) & 1u), kUniWGs);
+        }
+        pr.advance(P);
+        rc.next();
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------ math warpgroups
+    const int wg = warp >> 2;
+    const bool issuer = (warp & 3) == 0;
+    const uint32_t bar_id = 1 + wg;
+    const uint32_t op = tbase + kSlotCols * wg, acc = op + 32;
+    const uint32_t ta = tbase + lane_addr + kSlotCols * wg;
+    const uint32_t one = tbase + kUniOneCol;
+    const uint64_t dimg1 = tc::smem_desc_kmajor(tc::smem_u32(&S.img[0]), 512, 128);
+    const uint64_t dimg2 = tc::smem_desc_kmajor(tc::smem_u32(&S.img[0]), kN2 * 16, 128);
+    const bool adv = P.state_advanced != 0;
+    const float *beta = P.beta;
+    const float alpha_log2e = P.alpha * 1.4426950408889634f;
+    const float dsb = P.step->ds * P.beta_out;
+    const float decay = P.step->apply_decay != 0 ? P.step->decay : 1.0f;
+    const int n_peers = P.n_peers;
+    int32_t col_j = -1, col_b0 = -1;
+    int32_t a_img = -1, a_par = -1;
+    int red_j = -1;
+    float red_max = 0.0f, red_out = 0.0f;
+    Entry ce;
+    for (int32_t i = wg; i < nt; i += kUniWGs) {
+      const Pos<kUniRing> rc(i);
+      tc::mbar_wait(&S.full[rc.i], rc.phase);
+      const Stage &st = S.stage[rc.i];
+      const TileMeta &mt = st.meta;
+      const int32_t flags = mt.flags;
+      const int j = mt.j;
+      const bool valid = row >= mt.v0 && row < mt.v1;
+      if (mt.img != a_img || mt.img_par != a_par) {
+        tc::mbar_wait(&S.img_full[mt.img], (uint32_t)mt.img_par);
+        a_img = mt.img;
+        a_par = mt.img_par;
+      }
+      if (j != red_j) {
+        if (red_j >= 0) {
+          if (red_max > 0.0f)
+            atomicMax(reinterpret_cast<unsigned int *>(&P.maxabs[red_j]), __float_as_uint(red_max));
+          if (!(red_out <= 3.402823466e38f)) atomicOr(&P.status[red_j], LOPT_STATUS_NONFINITE_PARAM);
+        }
+        red_j = j;
+        red_max = 0.0f;
+        red_out = 0.0f;
+      }
+      const PrepImage &im = S.img[mt.img];
+      float4 *sp = mt.state + row;
+      float *tp = mt.theta + row;
+      float w, g;
+      float4 sq4;
+      if (!(flags & kFlagSlow)) {
+        w = st.th[row];
+        g = st.gr[row];
+        sq4 = st.st[row];
+      } else {
+        w = valid ? *tp : 0.0f;
+        g = valid ? mt.grad[row] : 0.0f;
+        sq4 = valid ? *sp : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      Entry re;
+      if (flags & kFlagRowblock) {
+        const uint4 v = st.rowent[0], hh = st.rowent[2], ll = st.rowent[3];
+        re.x[0] = __uint_as_float(v.x); re.x[1] = __uint_as_float(v.y); re.x[2] = __uint_as_float(v.z);
+        re.hi[0] = hh.x; re.hi[1] = hh.y; re.hi[2] = hh.z;
+        re.lo[0] = ll.x; re.lo[1] = ll.y; re.lo[2] = ll.z;
+        if (j != col_j || mt.b0 != col_b0) {
+          col_j = j;
+          col_b0 = mt.b0;
+          load_entry(mt.coltab, mt.b0 + row, ce);
+        }
+      } else {
+        const int32_t ec = mt.e0 + (valid ? row : (mt.v1 > mt.v0 ? mt.v0 : 0));
+        const int32_t la = (int32_t)((uint32_t)ec / (uint32_t)mt.n);
+        load_entry(mt.rowtab, la, re);
+        load_entry(mt.coltab, ec - la * mt.n, ce);
+        col_j = -1;
+      }
+      const uint64_t doff = (uint64_t)((uint32_t)mt.img * (uint32_t)(sizeof(PrepImage) >> 4));
+      FastIn x;
+      x.w = w;
+      advance(g, sq4, adv, beta, x);
+      // the accumulators do not depend on the MLP: store them right away
+      if (valid && !adv) *sp = make_float4(x.m1, x.m2, x.m3, x.v);
+      {
+        const float sq[3] = {im.sqmr[0], im.sqmr[1], im.sqmr[2]};
+        float f[16];
+        fast_features(x, re.x, ce.x, sq, f);
+        const float4 *es = reinterpret_cast<const float4 *>(im.escale);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const float4 e4 = es[q];
+          const float2 p0 = fmul2(make_float2(f[4 * q], f[4 * q + 1]), make_float2(e4.x, e4.y));
+          const float2 p1 = fmul2(make_float2(f[4 * q + 2], f[4 * q + 3]), make_float2(e4.z, e4.w));
+          f[4 * q] = p0.x; f[4 * q + 1] = p0.y; f[4 * q + 2] = p1.x; f[4 * q + 3] = p1.y;
+        }
+        uint32_t ev[16];
+#pragma unroll
+        for (int q = 0; q < 8; q++) split2(f[2 * q], f[2 * q + 1], ev[q], ev[8 + q]);
+        uint32_t xh = 0, xl = 0;
+        if (KIND == LOPT_VELO_MLP) split2(clip01(x.g) * im.escale[16], 0.0f, xh, xl);
+        uint32_t bv[16];
+        bv[0] = re.hi[0]; bv[1] = re.hi[1]; bv[2] = re.hi[2];
+        bv[3] = ce.hi[0]; bv[4] = ce.hi[1]; bv[5] = ce.hi[2];
+        bv[6] = (xh & 0xFFFFu) | 0x3C000000u;
+        bv[7] = 0u;
+        bv[8] = re.lo[0]; bv[9] = re.lo[1]; bv[10] = re.lo[2];
+        bv[11] = ce.lo[0]; bv[12] = ce.lo[1]; bv[13] = ce.lo[2];
+        bv[14] = xl & 0xFFFFu;
+        bv[15] = 0u;
+        tc::tmem_st16(ta, ev);
+        tc::tmem_st16(ta + 16, bv);
+        tc::tmem_st_wait();
+      }
+      tc::fence_before_sync();
+      if (issuer) {
+        tc::bar_sync(bar_id, 128);
+        tc::fence_after_sync();
+        if (tc::elect_one()) issue_layer1(dimg1 + doff, op, acc, &S.acc[wg]);
+        __syncwarp();
+      } else {
+        tc::bar_arrive(bar_id, 128);
+      }
+      tc::mbar_wait(&S.acc[wg], 0u);
+      tc::fence_after_sync();
+#pragma unroll
+      for (int half = 0; half < 2; half++) {
+        uint32_t h[16];
+        tc::tmem_ld16(ta + 32 + 16 * half, h);
+        tc::tmem_ld_wait();
+        uint32_t hi[8], lo[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          relu_split2(__uint_as_float(h[2 * q]), __uint_as_float(h[2 * q + 1]), hi[q], lo[q]);
+        tc::tmem_st8(ta + 8 * half, hi);
+        tc::tmem_st8(ta + 16 + 8 * half, lo);
+      }
+      tc::tmem_st_wait();
+      tc::fence_before_sync();
+      if (issuer) {
+        tc::bar_sync(bar_id, 128);
+        tc::fence_after_sync();
+        if (tc::elect_one()) issue_layer2(dimg2 + doff, op, acc, one, &S.acc[wg]);
+        __syncwarp();
+      } else {
+        tc::bar_arrive(bar_id, 128);
+      }
+      tc::mbar_wait(&S.acc[wg], 1u);
+      tc::fence_after_sync();
+      // layer 3 in f32: (b3 + linear half, from the MMA) + sum (w3/2)|h2|
+      const uint32_t tc2 = ta + 32;
+      uint32_t h2[16], lin[2];
+      tc::tmem_ld16(tc2, h2);
+      tc::tmem_ld2(tc2 + 32, lin);
+      tc::tmem_ld_wait();
+      float2 de = make_float2(__uint_as_float(lin[0]), __uint_as_float(lin[1]));
+      float2 dd = make_float2(0.0f, 0.0f);
+      const float4 *w3 = reinterpret_cast<const float4 *>(im.w3h);
+#pragma unroll
+      for (int half = 0; half < 2; half++) {
+        if (half == 1) {
+          tc::tmem_ld16(tc2 + 16, h2);
+          tc::tmem_ld_wait();
+        }
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const float4 wq = w3[8 * half + q];
+          const float he = fabsf(__uint_as_float(h2[2 * q])), ho = fabsf(__uint_as_float(h2[2 * q + 1]));
+          de = ffma2(make_float2(he, he), make_float2(wq.x, wq.y), de);
+          dd = ffma2(make_float2(ho, ho), make_float2(wq.z, wq.w), dd);
+        }
+      }
+      // the data slot and (for the producer's image reuse) this tile are done
+      mbar_arrive(&S.data_free[rc.i]);
+      __syncwarp();   // every lane's image reads precede lane 0's release
+      if ((flags & kFlagTail) && (threadIdx.x & 31) == 0)
+        asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&S.done[wg][warp & 3])),
+                     "r"(i)
+                     : "memory");
+      const float dir = de.x + dd.x, mag = de.y + dd.y;
+      const float du = dsb * (dir * ex2_ftz(mag * alpha_log2e));   // engine.py:537-539
+      const float out = (w + du) * decay;                          // optim.py:100-101
+      if (valid) {
+        red_max = fmaxf(red_max, fabsf(du));
+        red_out = max_nan_abs(red_out, out);
+        *tp = out;
+        for (int q = 0; q < n_peers; q++)
+          *reinterpret_cast<float *>(reinterpret_cast<char *>(tp) + P.peer_delta[q]) = out;
+      }
+    }
+    if (red_j >= 0) {
+      if (red_max > 0.0f)
+        atomicMax(reinterpret_cast<unsigned int *>(&P.maxabs[red_j]), __float_as_uint(red_max));
+      if (!(red_out <= 3.402823466e38f)) atomicOr(&P.status[red_j], LOPT_STATUS_NONFINITE_PARAM);
+    }
+    if (n_peers > 0) __threadfence_system();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, kTmemCols);
+}
+
 static int g_num_sms = 0;
 
 void launch_tc_apply(const DevicePlan &P0, cudaStream_t s) {
@@ -757,8 +1083,25 @@ void launch_tc_apply(const DevicePlan &P0, cudaStream_t s) {
     if (g_num_sms <= 0) g_num_sms = 148;
   }
   // one CTA per SM (the 512-column TMEM allocation needs it anyway)
-  const size_t smem = sizeof(ApplySmem) + 1024;
   const int grid = (int)std::min<int64_t>(g_num_sms, P.n_tiles);
+  static const int variant = [] {
+    const char *e = getenv("LOPT_APPLY_VARIANT");
+    return e ? atoi(e) : 2;
+  }();
+  if (variant == 2) {
+    const size_t smem = sizeof(UniSmem) + 1024;
+    if (P.kind == LOPT_SMALL_FC_LOPT) {
+      cudaFuncSetAttribute(apply_uni_kernel<LOPT_SMALL_FC_LOPT>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      apply_uni_kernel<LOPT_SMALL_FC_LOPT><<<grid, kUniThreads, smem, s>>>(P);
+    } else {
+      cudaFuncSetAttribute(apply_uni_kernel<LOPT_VELO_MLP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      apply_uni_kernel<LOPT_VELO_MLP><<<grid, kUniThreads, smem, s>>>(P);
+    }
+    return;
+  }
+  const size_t smem = sizeof(ApplySmem) + 1024;
   if (P.kind == LOPT_SMALL_FC_LOPT) {
     cudaFuncSetAttribute(apply_tc_kernel<LOPT_SMALL_FC_LOPT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
