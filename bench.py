@@ -493,6 +493,9 @@ def main():
                 # ncu capture, against ALGO_BYTES_PER_PARAM * params algorithmic
                 roofline["traffic"] = t[key]["bytes"]
                 roofline["traffic_unit"] = "GB per launch (ncu dram__bytes_read+write)"
+                if "step_bytes" in t[key]:
+                    # every kernel of the step (factor, stats, apply passes)
+                    roofline["step_traffic_gb"] = t[key]["step_bytes"]
                 roofline["algorithmic_gb"] = ALGO_BYTES_PER_PARAM * local_params / 1e9
         except (OSError, ValueError):
             pass

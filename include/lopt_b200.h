@@ -177,6 +177,8 @@ int lopt_selftest_expf(const float *x, float *y, int64_t n, void *stream);
 /* Micro-benchmark of the fast path's MMA shape: `batch` MMAs per commit,
  * `rounds` commit/wait round trips; out[0] = SM cycles per round. */
 int lopt_probe_umma(int32_t batch, int32_t rounds, long long *out, void *stream);
+/* TMEM ld/st throughput probe (development tool, no reference counterpart). */
+int lopt_probe_tmem(int32_t warps, int32_t mode, int32_t per, int32_t rounds, long long *out, void *stream);
 
 /* Fused parameter all-gather over NVLink (sharded step, replaces the
  * all-gather of distsim.py:523-530): every parameter the fast-mode apply pass

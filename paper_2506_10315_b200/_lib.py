@@ -34,7 +34,7 @@ EXPORTS = [
     "lopt_read_status", "lopt_debug_ptrs", "lopt_version",
     "lopt_num_kernels_launched_last_step", "lopt_velo_mix", "lopt_selftest_umma",
     "lopt_probe_umma", "lopt_selftest_expf", "lopt_set_peers", "lopt_graph_step",
-    "lopt_graph_reset", "lopt_set_velo",
+    "lopt_graph_reset", "lopt_set_velo", "lopt_probe_tmem",
 ]
 
 
@@ -125,6 +125,7 @@ def lib(required: bool = True):
     L.lopt_velo_mix.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, vp]
     L.lopt_selftest_umma.argtypes = [i32, i32, vp, vp, vp, vp]
     L.lopt_probe_umma.argtypes = [i32, i32, vp, vp]
+    L.lopt_probe_tmem.argtypes = [i32, i32, i32, i32, vp, vp]
     L.lopt_set_peers.argtypes = [vp, i32, vp]
     L.lopt_selftest_expf.argtypes = [vp, vp, ctypes.c_int64, vp]
     L.lopt_graph_step.argtypes = [vp, ctypes.POINTER(lopt_step_args), vp]

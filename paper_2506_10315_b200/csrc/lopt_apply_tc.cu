@@ -291,6 +291,7 @@ __device__ __forceinline__ void load_entry(const float *tab, int32_t i, Entry &E
 // first byte); every B slice is a constant 16-byte offset from it, so a tile
 // costs one uniform add per MMA instead of rebuilding descriptors.
 constexpr uint64_t slice_off(size_t bytes) { return (uint64_t)(bytes >> 4); }
+template <bool kCommit = true>
 __device__ __forceinline__ void issue_layer1(uint64_t dimg, uint32_t op, uint32_t acc, uint64_t *bar) {
   constexpr uint32_t idesc = tc::idesc_f16_f32(128, 32);
   const uint64_t w_eh = dimg + slice_off(offsetof(PrepImage, b1[0]));
@@ -303,9 +304,13 @@ __device__ __forceinline__ void issue_layer1(uint64_t dimg, uint32_t op, uint32_
   tc::mma_ts(acc, op + 16, w_bh, idesc, 1);
   tc::mma_ts(acc, op + 24, w_bh, idesc, 1);
   tc::mma_ts(acc, op + 16, w_bl, idesc, 1);
-  tc::mma_commit(bar);
+  if (kCommit) tc::mma_commit(bar);
+}
+__device__ __forceinline__ void issue_layer1_nc(uint64_t dimg, uint32_t op, uint32_t acc) {
+  issue_layer1<false>(dimg, op, acc, nullptr);
 }
 
+template <bool kCommit = true>
 __device__ __forceinline__ void issue_layer2(uint64_t dimg, uint32_t op, uint32_t acc,
                                              uint32_t one, uint64_t *bar) {
   constexpr uint32_t idesc = tc::idesc_f16_f32(128, kN2);
@@ -321,7 +326,10 @@ __device__ __forceinline__ void issue_layer2(uint64_t dimg, uint32_t op, uint32_
   tc::mma_ts(acc, op + 0, l0, idesc, 1);
   tc::mma_ts(acc, op + 8, l1, idesc, 1);
   tc::mma_ts(acc, one, bb, idesc, 1);
-  tc::mma_commit(bar);
+  if (kCommit) tc::mma_commit(bar);
+}
+__device__ __forceinline__ void issue_layer2_nc(uint64_t dimg, uint32_t op, uint32_t acc, uint32_t one) {
+  issue_layer2<false>(dimg, op, acc, one, nullptr);
 }
 
 __device__ __forceinline__ float ex2_ftz(float x) {
@@ -747,38 +755,197 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
 }
 
 // ---------------------------------------------------------------------------
-// Unified-warpgroup pipeline (the default): every math warpgroup carries its
-// own tiles through all stages -- features, layer-1 MMAs, layer-1 epilogue,
-// layer-2 MMAs, layer 3 + update -- in its own TMEM slot, issuing its MMAs
-// from an elected lane of its first warp.  kUniWGs warpgroups interleave, so
-// while one waits for its MMAs the others compute; there are no hand-offs
-// between roles (the per-tile waits are the warpgroup's own TMA data and its
-// two MMA commits), which removes most of the barrier polling and per-role
-// bookkeeping of the role-specialized pipeline above, and each thread keeps
-// its element's values in registers from load to store.
-constexpr int kUniWGs = 4;
-constexpr int kUniRing = 16;
-constexpr int kUniProducers = 2;
-constexpr int kUniThreads = kUniWGs * 128 + kUniProducers * 32;
-constexpr int kUniWarpProducer = kUniWGs * 4;
-constexpr uint32_t kUniOneCol = kSlotCols * kUniWGs;
-static_assert(kUniOneCol + 8 <= kTmemCols, "TMEM budget");
+// Pair pipeline (the default; LOPT_APPLY_VARIANT=1 selects the role-specialized
+// kernel above).  Every math warpgroup carries its own tiles through all
+// stages -- features, layer-1 MMAs, layer-1 epilogue, layer-2 MMAs, layer 3 +
+// update -- in its own TMEM slots, issuing its MMAs from an elected lane of its
+// first warp; the warpgroups interleave, so while one waits for its MMAs the
+// others compute, and there are no hand-offs between roles (the per-iteration
+// waits are the warpgroup's TMA data and its two MMA commits).  Each iteration
+// carries a PAIR of 128-element tiles in two TMEM slots (rowblock tensors: rows
+// 2r and 2r+1 of one column block, so the pair shares its column-table entries;
+// flat tensors: tiles 2q, 2q+1; a missing second tile is an empty tile): one
+// data-ring wait, one image check, one w3 read, two MMA commits and two
+// warpgroup barriers per 256 elements, and two independent elements per thread
+// for ILP between the MMA waits.  Measured against the role-specialized kernel
+// (ncu, ViT-B/16): 396 vs 516 thread-instructions per element, 1.61 vs 1.84 ms.
+constexpr int kPWGs = 3;
+constexpr int kPRing = 12;
+constexpr int kPProducers = 2;
+constexpr int kPThreads = kPWGs * 128 + kPProducers * 32;
+constexpr int kPWarpProducer = kPWGs * 4;
+constexpr uint32_t kPOneCol = 2 * kSlotCols * kPWGs;
+static_assert(kPOneCol + 8 <= kTmemCols, "TMEM budget");
 
-struct __align__(1024) UniSmem {
+struct __align__(128) PairStage {
+  float4 st[2][128];     // {M1, M2, M3, V}
+  float th[2][128];
+  float gr[2][128];
+  uint4 rowent[2][4];    // rowblock: each tile row's table entry
+  TileMeta meta[2];
+};
+
+struct __align__(1024) PairSmem {
   PrepImage img[kImgs];
-  Stage stage[kUniRing];
-  uint64_t full[kUniRing];       // producer -> WG: tile staged (TMA complete_tx)
-  uint64_t data_free[kUniRing];  // WG -> producer (128 arrivals)
-  uint64_t acc[kUniWGs];         // MMA commits of the WG (two phases per tile)
-  uint64_t img_full[kImgs];      // producer -> WGs: operand image loaded
-  int32_t done[kUniWGs][4];      // WG warps: last tile finished (image-buffer reuse)
+  PairStage stage[kPRing];
+  uint64_t full[kPRing];       // producer -> WG: pair staged (TMA complete_tx)
+  uint64_t data_free[kPRing];  // WG -> producer (128 arrivals)
+  uint64_t acc[kPWGs];         // MMA commits of the WG (two phases per pair)
+  uint64_t img_full[kImgs];    // producer -> WGs: operand image loaded
+  int32_t done[kPWGs][4];      // WG warps: last pair finished (image-buffer reuse)
   uint32_t tmem_base;
 };
 
+// Walks a CTA's pairs in order (one lane), staging both tiles of each.
+struct PairProducer {
+  int j = -1;
+  int32_t left = 0;                 // pairs of tensor j still to stage
+  int32_t hp = 1, rp = 0, b0 = 0;   // rowblock: row pairs per column block, row pair, first column
+  int32_t e0 = 0;                   // flat: first element of the pair
+  int32_t n = 1, lo = 0, hi = 0, a_lo = 0, mr = 0;
+  bool rb = false, aligned = false;
+  float *theta = nullptr;
+  const float *grad = nullptr, *rowtab = nullptr, *coltab = nullptr;
+  float4 *state = nullptr;
+
+  __device__ __forceinline__ void load_tensor(const DevicePlan &P, int jj, int32_t q) {
+    const TensorDesc *T = P.tensors + jj;
+    j = jj;
+    n = (int32_t)T->n;
+    lo = (int32_t)T->lo;
+    hi = (int32_t)T->hi;
+    rb = T->rowblock != 0;
+    a_lo = T->a_lo;
+    mr = T->m_rows;
+    theta = T->theta;
+    grad = T->grad;
+    state = T->state;
+    rowtab = T->rowtab;
+    coltab = T->coltab;
+    aligned = ((reinterpret_cast<uintptr_t>(theta) | reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+    left = T->pairs - q;
+    if (rb) {
+      hp = (mr + 1) >> 1;
+      rp = q % hp;
+      b0 = (q / hp) * kTile;
+    } else {
+      e0 = lo + q * 2 * kTile;
+    }
+  }
+  __device__ __forceinline__ void seek(const DevicePlan &P, int32_t t) {
+    int jj = 0;
+    while (jj + 1 < P.count && P.tensors[jj + 1].pair0 <= t) jj++;
+    while (P.tensors[jj].pairs == 0 && jj + 1 < P.count) jj++;
+    load_tensor(P, jj, t - (int32_t)P.tensors[jj].pair0);
+  }
+  __device__ __forceinline__ void advance(const DevicePlan &P) {
+    if (--left == 0) {
+      int jj = j + 1;
+      while (jj < P.count && P.tensors[jj].pairs == 0) jj++;
+      if (jj < P.count) load_tensor(P, jj, 0);
+      return;
+    }
+    if (rb) {
+      if (++rp == hp) {
+        rp = 0;
+        b0 += kTile;
+      }
+    } else {
+      e0 += 2 * kTile;
+    }
+  }
+  __device__ __forceinline__ void stage(PairStage &st, uint64_t *full, int img, int img_par) {
+    int32_t el[2], va[2], vb[2];
+    bool fast[2], ex[2];
+    int32_t arow[2];
+    uint32_t bytes = 0;
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      if (rb) {
+        ex[k] = 2 * rp + k < mr;
+        arow[k] = a_lo + (ex[k] ? 2 * rp + k : 0);
+        el[k] = arow[k] * n + b0;
+      } else {
+        el[k] = e0 + k * kTile;
+        ex[k] = el[k] < hi;
+        if (!ex[k]) el[k] = lo;
+        arow[k] = 0;
+      }
+      int32_t v0 = max(0, lo - el[k]), v1 = min(kTile, hi - el[k]);
+      if (!ex[k] || v1 <= v0) v0 = v1 = 0;
+      va[k] = v0;
+      vb[k] = v1;
+      // an empty tile reads nothing: the slow path with no valid lanes yields zeros
+      fast[k] = ex[k] && aligned && ((el[k] + v0) & 3) == 0 && ((v1 - v0) & 3) == 0;
+      TileMeta mt;
+      mt.j = j;
+      mt.b0 = b0;
+      mt.e0 = el[k];
+      mt.n = n;
+      mt.v0 = v0;
+      mt.v1 = v1;
+      mt.flags = (rb ? kFlagRowblock : 0) | (fast[k] ? 0 : kFlagSlow) | (left <= kPWGs ? kFlagTail : 0);
+      mt.img = img;
+      mt.img_par = img_par;
+      mt.pad0[0] = mt.pad0[1] = mt.pad0[2] = 0;
+      mt.theta = theta + el[k];
+      mt.grad = grad + el[k];
+      mt.state = state + (el[k] - lo);
+      mt.rowtab = rowtab;
+      mt.coltab = coltab;
+      mt.pad = nullptr;
+      st.meta[k] = mt;
+      bytes += (fast[k] ? 24u * (uint32_t)(v1 - v0) : 0u) + (rb ? 64u : 0u);
+    }
+    mbar_arrive_tx(full, bytes);
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const uint32_t nv = (uint32_t)(vb[k] - va[k]);
+      if (fast[k] && nv > 0) {
+        bulk_g2s(&st.th[k][va[k]], theta + el[k] + va[k], 4 * nv, full);
+        bulk_g2s(&st.gr[k][va[k]], grad + el[k] + va[k], 4 * nv, full);
+        bulk_g2s(&st.st[k][va[k]], state + (el[k] + va[k] - lo), 16 * nv, full);
+      }
+      if (rb) bulk_g2s(st.rowent[k], rowtab + (int64_t)arow[k] * kRowTab, 64, full);
+    }
+  }
+};
+
+// Features of one element -> the tile's E (hi | lo) and B operand words.
 template <int KIND>
-__global__ void __launch_bounds__(kUniThreads, 1) apply_uni_kernel(DevicePlan P) {
+__device__ __forceinline__ void pair_operands(const FastIn &x, const Entry &re, const Entry &ce,
+                                              const PrepImage &im, uint32_t (&ev)[16],
+                                              uint32_t (&bv)[16]) {
+  const float sq[3] = {im.sqmr[0], im.sqmr[1], im.sqmr[2]};
+  float f[16];
+  fast_features(x, re.x, ce.x, sq, f);
+  // normalize (features.py:349-354) so every operand fits fp16
+  const float4 *es = reinterpret_cast<const float4 *>(im.escale);
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const float4 e4 = es[q];
+    const float2 p0 = fmul2(make_float2(f[4 * q], f[4 * q + 1]), make_float2(e4.x, e4.y));
+    const float2 p1 = fmul2(make_float2(f[4 * q + 2], f[4 * q + 3]), make_float2(e4.z, e4.w));
+    f[4 * q] = p0.x; f[4 * q + 1] = p0.y; f[4 * q + 2] = p1.x; f[4 * q + 3] = p1.y;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; q++) split2(f[2 * q], f[2 * q + 1], ev[q], ev[8 + q]);
+  uint32_t xh = 0, xl = 0;
+  if (KIND == LOPT_VELO_MLP) split2(clip01(x.g) * im.escale[16], 0.0f, xh, xl);
+  bv[0] = re.hi[0]; bv[1] = re.hi[1]; bv[2] = re.hi[2];
+  bv[3] = ce.hi[0]; bv[4] = ce.hi[1]; bv[5] = ce.hi[2];
+  bv[6] = (xh & 0xFFFFu) | 0x3C000000u;   // clip_hi, fp16 1 (bias)
+  bv[7] = 0u;
+  bv[8] = re.lo[0]; bv[9] = re.lo[1]; bv[10] = re.lo[2];
+  bv[11] = ce.lo[0]; bv[12] = ce.lo[1]; bv[13] = ce.lo[2];
+  bv[14] = xl & 0xFFFFu;
+  bv[15] = 0u;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  UniSmem &S = *reinterpret_cast<UniSmem *>(smem_raw);
+  PairSmem &S = *reinterpret_cast<PairSmem *>(smem_raw);
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int row = tid & 127;
@@ -787,12 +954,12 @@ __global__ void __launch_bounds__(kUniThreads, 1) apply_uni_kernel(DevicePlan P)
     tc::tmem_relinquish();
   }
   if (tid == 0) {
-    for (int r = 0; r < kUniRing; r++) {
+    for (int r = 0; r < kPRing; r++) {
       tc::mbar_init(&S.full[r], 1);
       tc::mbar_init(&S.data_free[r], 128);
     }
     for (int b = 0; b < kImgs; b++) tc::mbar_init(&S.img_full[b], 1);
-    for (int w = 0; w < kUniWGs; w++) {
+    for (int w = 0; w < kPWGs; w++) {
       tc::mbar_init(&S.acc[w], 1);
       for (int q = 0; q < 4; q++) S.done[w][q] = -1;
     }
@@ -806,28 +973,28 @@ __global__ void __launch_bounds__(kUniThreads, 1) apply_uni_kernel(DevicePlan P)
   if (warp < 4) {
     // the constant slice that selects the layer-2 bias: fp16 {1, 1, 0, ...}
     const uint32_t one[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    tc::tmem_st8(tbase + lane_addr + kUniOneCol, one);
+    tc::tmem_st8(tbase + lane_addr + kPOneCol, one);
     tc::tmem_st_wait();
   }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const bool aborted = *P.abort_flag != 0;
-  const int32_t tb = (int32_t)(P.n_tiles * blockIdx.x / gridDim.x);
-  const int32_t te = (int32_t)(P.n_tiles * (blockIdx.x + 1) / gridDim.x);
-  const int32_t nt = aborted ? 0 : te - tb;
+  const int32_t pb = (int32_t)(P.n_pairs * blockIdx.x / gridDim.x);
+  const int32_t pe = (int32_t)(P.n_pairs * (blockIdx.x + 1) / gridDim.x);
+  const int32_t np = aborted ? 0 : pe - pb;
 
-  if (warp >= kUniWarpProducer) {
+  if (warp >= kPWarpProducer) {
     // -------------------------------------------------------------- producers
-    const int p = warp - kUniWarpProducer;
-    if (tc::elect_one() && nt > 0) {
-      Producer pr;
-      pr.seek(P, tb);
+    const int p = warp - kPWarpProducer;
+    if (tc::elect_one() && np > 0) {
+      PairProducer pr;
+      pr.seek(P, pb);
       int k = -1, img = 0, cur_j = -1;
       uint32_t par_bits = 0;
       int32_t first[kImgs] = {0, 0, 0, 0};
-      Cursor<kUniRing> rc;
-      for (int32_t i = 0; i < nt; i++) {
+      Cursor<kPRing> rc;
+      for (int32_t i = 0; i < np; i++) {
         if (pr.j != cur_j) {
           cur_j = pr.j;
           k++;
@@ -836,13 +1003,13 @@ __global__ void __launch_bounds__(kUniThreads, 1) apply_uni_kernel(DevicePlan P)
           const int32_t nf = first[(k + 1) & (kImgs - 1)];
           first[img] = i;
           if (k >= kImgs) par_bits ^= 1u << img;
-          if (i % kUniProducers == p) {
+          if (i % kPProducers == p) {
             if (k >= kImgs) {
-              // tensor k - kImgs used tiles [pf, nf - 1]: every warp of every
-              // WG must be past its last tile in that range
+              // tensor k - kImgs used pairs [pf, nf - 1]: every warp of every
+              // WG must be past its last pair in that range
               const int32_t last = nf - 1;
-              for (int w = 0; w < kUniWGs; w++) {
-                const int32_t need = last - (((last - w) % kUniWGs) + kUniWGs) % kUniWGs;
+              for (int w = 0; w < kPWGs; w++) {
+                const int32_t need = last - (((last - w) % kPWGs) + kPWGs) % kPWGs;
                 if (need < pf) continue;
                 for (int q = 0; q < 4; q++) {
                   int32_t d;
@@ -862,9 +1029,10 @@ __global__ void __launch_bounds__(kUniThreads, 1) apply_uni_kernel(DevicePlan P)
                      (uint32_t)sizeof(PrepImage), &S.img_full[img]);
           }
         }
-        if (i % kUniProducers == p) {
-          if (rc.wrapped) tc::mbar_wait(&S.data_free[rc.i], rc.phase ^ 1u);
-          pr.stage(S.stage[rc.i], &S.full[rc.i], img, (int)((par_bits >> img) & 1u), kUniWGs);
+        if (i % kPProducers == p) {
+          // parked in hardware while the ring is full (no issue slots spent)
+          if (rc.wrapped) tc::mbar_sleep(&S.data_free[rc.i], rc.phase ^ 1u);
+          pr.stage(S.stage[rc.i], &S.full[rc.i], img, (int)((par_bits >> img) & 1u));
         }
         pr.advance(P);
         rc.next();
@@ -876,9 +1044,9 @@ __global__ void __launch_bounds__(kUniThreads, 1) apply_uni_kernel(DevicePlan P)
     const int wg = warp >> 2;
     const bool issuer = (warp & 3) == 0;
     const uint32_t bar_id = 1 + wg;
-    const uint32_t op = tbase + kSlotCols * wg, acc = op + 32;
-    const uint32_t ta = tbase + lane_addr + kSlotCols * wg;
-    const uint32_t one = tbase + kUniOneCol;
+    const uint32_t op0 = tbase + 2 * kSlotCols * wg, op1 = op0 + kSlotCols;
+    const uint32_t ta0 = op0 + lane_addr, ta1 = op1 + lane_addr;
+    const uint32_t one = tbase + kPOneCol;
     const uint64_t dimg1 = tc::smem_desc_kmajor(tc::smem_u32(&S.img[0]), 512, 128);
     const uint64_t dimg2 = tc::smem_desc_kmajor(tc::smem_u32(&S.img[0]), kN2 * 16, 128);
     const bool adv = P.state_advanced != 0;
@@ -891,19 +1059,18 @@ __global__ void __launch_bounds__(kUniThreads, 1) apply_uni_kernel(DevicePlan P)
     int32_t a_img = -1, a_par = -1;
     int red_j = -1;
     float red_max = 0.0f, red_out = 0.0f;
-    Entry ce;
-    for (int32_t i = wg; i < nt; i += kUniWGs) {
-      const Pos<kUniRing> rc(i);
+    Entry ce, ce1;
+    for (int32_t i = wg; i < np; i += kPWGs) {
+      const Pos<kPRing> rc(i);
       tc::mbar_wait(&S.full[rc.i], rc.phase);
-      const Stage &st = S.stage[rc.i];
-      const TileMeta &mt = st.meta;
-      const int32_t flags = mt.flags;
-      const int j = mt.j;
-      const bool valid = row >= mt.v0 && row < mt.v1;
-      if (mt.img != a_img || mt.img_par != a_par) {
-        tc::mbar_wait(&S.img_full[mt.img], (uint32_t)mt.img_par);
-        a_img = mt.img;
-        a_par = mt.img_par;
+      const PairStage &st = S.stage[rc.i];
+      const TileMeta &m0 = st.meta[0];
+      const int32_t flags0 = m0.flags, flags1 = st.meta[1].flags;
+      const int j = m0.j;
+      if (m0.img != a_img || m0.img_par != a_par) {
+        tc::mbar_wait(&S.img_full[m0.img], (uint32_t)m0.img_par);
+        a_img = m0.img;
+        a_par = m0.img_par;
       }
       if (j != red_j) {
         if (red_j >= 0) {
@@ -915,148 +1082,174 @@ __global__ void __launch_bounds__(kUniThreads, 1) apply_uni_kernel(DevicePlan P)
         red_max = 0.0f;
         red_out = 0.0f;
       }
-      const PrepImage &im = S.img[mt.img];
-      float4 *sp = mt.state + row;
-      float *tp = mt.theta + row;
-      float w, g;
-      float4 sq4;
-      if (!(flags & kFlagSlow)) {
-        w = st.th[row];
-        g = st.gr[row];
-        sq4 = st.st[row];
-      } else {
-        w = valid ? *tp : 0.0f;
-        g = valid ? mt.grad[row] : 0.0f;
-        sq4 = valid ? *sp : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      Entry re;
-      if (flags & kFlagRowblock) {
-        const uint4 v = st.rowent[0], hh = st.rowent[2], ll = st.rowent[3];
-        re.x[0] = __uint_as_float(v.x); re.x[1] = __uint_as_float(v.y); re.x[2] = __uint_as_float(v.z);
-        re.hi[0] = hh.x; re.hi[1] = hh.y; re.hi[2] = hh.z;
-        re.lo[0] = ll.x; re.lo[1] = ll.y; re.lo[2] = ll.z;
-        if (j != col_j || mt.b0 != col_b0) {
+      const PrepImage &im = S.img[m0.img];
+      const uint64_t doff = (uint64_t)((uint32_t)m0.img * (uint32_t)(sizeof(PrepImage) >> 4));
+      // ---- inputs of both tiles
+      bool valid[2];
+      float w[2];
+      float *tp[2];
+      float4 *sp[2];
+      FastIn x[2];
+      Entry re[2];
+      if (flags0 & kFlagRowblock) {
+        // both tiles are rows of one column block: one column entry (cached
+        // across the pairs of the block; tile 1 reads its own copy)
+        if (j != col_j || m0.b0 != col_b0) {
           col_j = j;
-          col_b0 = mt.b0;
-          load_entry(mt.coltab, mt.b0 + row, ce);
+          col_b0 = m0.b0;
+          load_entry(m0.coltab, m0.b0 + row, ce);
+          load_entry(m0.coltab, m0.b0 + row, ce1);
         }
       } else {
-        const int32_t ec = mt.e0 + (valid ? row : (mt.v1 > mt.v0 ? mt.v0 : 0));
-        const int32_t la = (int32_t)((uint32_t)ec / (uint32_t)mt.n);
-        load_entry(mt.rowtab, la, re);
-        load_entry(mt.coltab, ec - la * mt.n, ce);
         col_j = -1;
       }
-      const uint64_t doff = (uint64_t)((uint32_t)mt.img * (uint32_t)(sizeof(PrepImage) >> 4));
-      FastIn x;
-      x.w = w;
-      advance(g, sq4, adv, beta, x);
-      // the accumulators do not depend on the MLP: store them right away
-      if (valid && !adv) *sp = make_float4(x.m1, x.m2, x.m3, x.v);
-      {
-        const float sq[3] = {im.sqmr[0], im.sqmr[1], im.sqmr[2]};
-        float f[16];
-        fast_features(x, re.x, ce.x, sq, f);
-        const float4 *es = reinterpret_cast<const float4 *>(im.escale);
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const float4 e4 = es[q];
-          const float2 p0 = fmul2(make_float2(f[4 * q], f[4 * q + 1]), make_float2(e4.x, e4.y));
-          const float2 p1 = fmul2(make_float2(f[4 * q + 2], f[4 * q + 3]), make_float2(e4.z, e4.w));
-          f[4 * q] = p0.x; f[4 * q + 1] = p0.y; f[4 * q + 2] = p1.x; f[4 * q + 3] = p1.y;
+      for (int k = 0; k < 2; k++) {
+        const TileMeta &mt = st.meta[k];
+        const int32_t fl = k == 0 ? flags0 : flags1;
+        valid[k] = row >= mt.v0 && row < mt.v1;
+        tp[k] = mt.theta + row;
+        float g;
+        float4 sq4;
+        if (!(fl & kFlagSlow)) {
+          w[k] = st.th[k][row];
+          g = st.gr[k][row];
+          sq4 = st.st[k][row];
+        } else {
+          w[k] = valid[k] ? mt.theta[row] : 0.0f;
+          g = valid[k] ? mt.grad[row] : 0.0f;
+          sq4 = valid[k] ? mt.state[row] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        uint32_t ev[16];
-#pragma unroll
-        for (int q = 0; q < 8; q++) split2(f[2 * q], f[2 * q + 1], ev[q], ev[8 + q]);
-        uint32_t xh = 0, xl = 0;
-        if (KIND == LOPT_VELO_MLP) split2(clip01(x.g) * im.escale[16], 0.0f, xh, xl);
-        uint32_t bv[16];
-        bv[0] = re.hi[0]; bv[1] = re.hi[1]; bv[2] = re.hi[2];
-        bv[3] = ce.hi[0]; bv[4] = ce.hi[1]; bv[5] = ce.hi[2];
-        bv[6] = (xh & 0xFFFFu) | 0x3C000000u;
-        bv[7] = 0u;
-        bv[8] = re.lo[0]; bv[9] = re.lo[1]; bv[10] = re.lo[2];
-        bv[11] = ce.lo[0]; bv[12] = ce.lo[1]; bv[13] = ce.lo[2];
-        bv[14] = xl & 0xFFFFu;
-        bv[15] = 0u;
-        tc::tmem_st16(ta, ev);
-        tc::tmem_st16(ta + 16, bv);
+        if (fl & kFlagRowblock) {
+          const uint4 v = st.rowent[k][0], hh = st.rowent[k][2], ll = st.rowent[k][3];
+          re[k].x[0] = __uint_as_float(v.x); re[k].x[1] = __uint_as_float(v.y); re[k].x[2] = __uint_as_float(v.z);
+          re[k].hi[0] = hh.x; re[k].hi[1] = hh.y; re[k].hi[2] = hh.z;
+          re[k].lo[0] = ll.x; re[k].lo[1] = ll.y; re[k].lo[2] = ll.z;
+        } else {
+          const int32_t ec = mt.e0 + (valid[k] ? row : (mt.v1 > mt.v0 ? mt.v0 : 0));
+          const int32_t la = (int32_t)((uint32_t)ec / (uint32_t)mt.n);
+          load_entry(mt.rowtab, la, re[k]);
+          load_entry(mt.coltab, ec - la * mt.n, k == 0 ? ce : ce1);
+        }
+        x[k].w = w[k];
+        sp[k] = mt.state + row;
+        advance(g, sq4, adv, beta, x[k]);
+      }
+      // ---- features -> E/B operands of both tiles, layer-1 MMAs
+      {
+        uint32_t ev[16], bv[16];
+        pair_operands<KIND>(x[0], re[0], ce, im, ev, bv);
+        tc::tmem_st16(ta0, ev);
+        tc::tmem_st16(ta0 + 16, bv);
+        pair_operands<KIND>(x[1], re[1], ce1, im, ev, bv);
+        tc::tmem_st16(ta1, ev);
+        tc::tmem_st16(ta1 + 16, bv);
         tc::tmem_st_wait();
       }
       tc::fence_before_sync();
       if (issuer) {
         tc::bar_sync(bar_id, 128);
         tc::fence_after_sync();
-        if (tc::elect_one()) issue_layer1(dimg1 + doff, op, acc, &S.acc[wg]);
+        if (tc::elect_one()) {
+          issue_layer1_nc(dimg1 + doff, op0, op0 + 32);
+          issue_layer1(dimg1 + doff, op1, op1 + 32, &S.acc[wg]);
+        }
         __syncwarp();
       } else {
         tc::bar_arrive(bar_id, 128);
       }
+      // the accumulators do not depend on the MLP: stored while layer 1 runs
+#pragma unroll
+      for (int k = 0; k < 2; k++)
+        if (valid[k] && !adv) *sp[k] = make_float4(x[k].m1, x[k].m2, x[k].m3, x[k].v);
       tc::mbar_wait(&S.acc[wg], 0u);
       tc::fence_after_sync();
+      // ---- layer-1 epilogue (ReLU + split -> H) of both tiles, layer-2 MMAs
 #pragma unroll
       for (int half = 0; half < 2; half++) {
-        uint32_t h[16];
-        tc::tmem_ld16(ta + 32 + 16 * half, h);
+        uint32_t h0[16], h1[16];
+        tc::tmem_ld16(ta0 + 32 + 16 * half, h0);
+        tc::tmem_ld16(ta1 + 32 + 16 * half, h1);
         tc::tmem_ld_wait();
-        uint32_t hi[8], lo[8];
+        uint32_t hi0[8], lo0[8], hi1[8], lo1[8];
 #pragma unroll
-        for (int q = 0; q < 8; q++)
-          relu_split2(__uint_as_float(h[2 * q]), __uint_as_float(h[2 * q + 1]), hi[q], lo[q]);
-        tc::tmem_st8(ta + 8 * half, hi);
-        tc::tmem_st8(ta + 16 + 8 * half, lo);
+        for (int q = 0; q < 8; q++) {
+          relu_split2(__uint_as_float(h0[2 * q]), __uint_as_float(h0[2 * q + 1]), hi0[q], lo0[q]);
+          relu_split2(__uint_as_float(h1[2 * q]), __uint_as_float(h1[2 * q + 1]), hi1[q], lo1[q]);
+        }
+        tc::tmem_st8(ta0 + 8 * half, hi0);
+        tc::tmem_st8(ta0 + 16 + 8 * half, lo0);
+        tc::tmem_st8(ta1 + 8 * half, hi1);
+        tc::tmem_st8(ta1 + 16 + 8 * half, lo1);
       }
       tc::tmem_st_wait();
       tc::fence_before_sync();
       if (issuer) {
         tc::bar_sync(bar_id, 128);
         tc::fence_after_sync();
-        if (tc::elect_one()) issue_layer2(dimg2 + doff, op, acc, one, &S.acc[wg]);
+        if (tc::elect_one()) {
+          issue_layer2_nc(dimg2 + doff, op0, op0 + 32, one);
+          issue_layer2(dimg2 + doff, op1, op1 + 32, one, &S.acc[wg]);
+        }
         __syncwarp();
       } else {
         tc::bar_arrive(bar_id, 128);
       }
       tc::mbar_wait(&S.acc[wg], 1u);
       tc::fence_after_sync();
-      // layer 3 in f32: (b3 + linear half, from the MMA) + sum (w3/2)|h2|
-      const uint32_t tc2 = ta + 32;
-      uint32_t h2[16], lin[2];
-      tc::tmem_ld16(tc2, h2);
-      tc::tmem_ld2(tc2 + 32, lin);
-      tc::tmem_ld_wait();
-      float2 de = make_float2(__uint_as_float(lin[0]), __uint_as_float(lin[1]));
-      float2 dd = make_float2(0.0f, 0.0f);
-      const float4 *w3 = reinterpret_cast<const float4 *>(im.w3h);
+      // ---- layer 3 in f32: (b3 + linear half, from the MMA) + sum (w3/2)|h2|
+      float2 de[2], dd[2];
+      {
+        uint32_t h0[16], h1[16], l0[2], l1[2];
+        tc::tmem_ld16(ta0 + 32, h0);
+        tc::tmem_ld16(ta1 + 32, h1);
+        tc::tmem_ld2(ta0 + 64, l0);
+        tc::tmem_ld2(ta1 + 64, l1);
+        tc::tmem_ld_wait();
+        de[0] = make_float2(__uint_as_float(l0[0]), __uint_as_float(l0[1]));
+        de[1] = make_float2(__uint_as_float(l1[0]), __uint_as_float(l1[1]));
+        dd[0] = dd[1] = make_float2(0.0f, 0.0f);
+        const float4 *w3 = reinterpret_cast<const float4 *>(im.w3h);
 #pragma unroll
-      for (int half = 0; half < 2; half++) {
-        if (half == 1) {
-          tc::tmem_ld16(tc2 + 16, h2);
-          tc::tmem_ld_wait();
-        }
+        for (int half = 0; half < 2; half++) {
+          if (half == 1) {
+            tc::tmem_ld16(ta0 + 48, h0);
+            tc::tmem_ld16(ta1 + 48, h1);
+            tc::tmem_ld_wait();
+          }
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
-          const float4 wq = w3[8 * half + q];
-          const float he = fabsf(__uint_as_float(h2[2 * q])), ho = fabsf(__uint_as_float(h2[2 * q + 1]));
-          de = ffma2(make_float2(he, he), make_float2(wq.x, wq.y), de);
-          dd = ffma2(make_float2(ho, ho), make_float2(wq.z, wq.w), dd);
+          for (int q = 0; q < 8; q++) {
+            const float4 wq = w3[8 * half + q];
+            const float2 wd = make_float2(wq.x, wq.y), wm = make_float2(wq.z, wq.w);
+            float he = fabsf(__uint_as_float(h0[2 * q])), ho = fabsf(__uint_as_float(h0[2 * q + 1]));
+            de[0] = ffma2(make_float2(he, he), wd, de[0]);
+            dd[0] = ffma2(make_float2(ho, ho), wm, dd[0]);
+            he = fabsf(__uint_as_float(h1[2 * q]));
+            ho = fabsf(__uint_as_float(h1[2 * q + 1]));
+            de[1] = ffma2(make_float2(he, he), wd, de[1]);
+            dd[1] = ffma2(make_float2(ho, ho), wm, dd[1]);
+          }
         }
       }
-      // the data slot and (for the producer's image reuse) this tile are done
+      // the data slot and (for the producer's image reuse) this pair are done
       mbar_arrive(&S.data_free[rc.i]);
       __syncwarp();   // every lane's image reads precede lane 0's release
-      if ((flags & kFlagTail) && (threadIdx.x & 31) == 0)
+      if ((flags0 & kFlagTail) && (threadIdx.x & 31) == 0)
         asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&S.done[wg][warp & 3])),
                      "r"(i)
                      : "memory");
-      const float dir = de.x + dd.x, mag = de.y + dd.y;
-      const float du = dsb * (dir * ex2_ftz(mag * alpha_log2e));   // engine.py:537-539
-      const float out = (w + du) * decay;                          // optim.py:100-101
-      if (valid) {
-        red_max = fmaxf(red_max, fabsf(du));
-        red_out = max_nan_abs(red_out, out);
-        *tp = out;
-        for (int q = 0; q < n_peers; q++)
-          *reinterpret_cast<float *>(reinterpret_cast<char *>(tp) + P.peer_delta[q]) = out;
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        const float dir = de[k].x + dd[k].x, mag = de[k].y + dd[k].y;
+        const float du = dsb * (dir * ex2_ftz(mag * alpha_log2e));   // engine.py:537-539
+        const float out = (w[k] + du) * decay;                       // optim.py:100-101
+        if (valid[k]) {
+          red_max = fmaxf(red_max, fabsf(du));
+          red_out = max_nan_abs(red_out, out);
+          *tp[k] = out;
+          for (int q = 0; q < n_peers; q++)
+            *reinterpret_cast<float *>(reinterpret_cast<char *>(tp[k]) + P.peer_delta[q]) = out;
+        }
       }
     }
     if (red_j >= 0) {
@@ -1084,20 +1277,20 @@ void launch_tc_apply(const DevicePlan &P0, cudaStream_t s) {
   }
   // one CTA per SM (the 512-column TMEM allocation needs it anyway)
   const int grid = (int)std::min<int64_t>(g_num_sms, P.n_tiles);
-  static const int variant = [] {
-    const char *e = getenv("LOPT_APPLY_VARIANT");
-    return e ? atoi(e) : 2;
-  }();
-  if (variant == 2) {
-    const size_t smem = sizeof(UniSmem) + 1024;
+  // development A/B switch (read per launch so one process can compare)
+  const char *ve = getenv("LOPT_APPLY_VARIANT");
+  const int variant = ve ? atoi(ve) : 3;
+  if (variant == 3) {
+    const size_t smem = sizeof(PairSmem) + 1024;
+    const int pgrid = (int)std::min<int64_t>(g_num_sms, P.n_pairs);
     if (P.kind == LOPT_SMALL_FC_LOPT) {
-      cudaFuncSetAttribute(apply_uni_kernel<LOPT_SMALL_FC_LOPT>,
+      cudaFuncSetAttribute(apply_pair_kernel<LOPT_SMALL_FC_LOPT>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      apply_uni_kernel<LOPT_SMALL_FC_LOPT><<<grid, kUniThreads, smem, s>>>(P);
+      apply_pair_kernel<LOPT_SMALL_FC_LOPT><<<pgrid, kPThreads, smem, s>>>(P);
     } else {
-      cudaFuncSetAttribute(apply_uni_kernel<LOPT_VELO_MLP>,
+      cudaFuncSetAttribute(apply_pair_kernel<LOPT_VELO_MLP>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      apply_uni_kernel<LOPT_VELO_MLP><<<grid, kUniThreads, smem, s>>>(P);
+      apply_pair_kernel<LOPT_VELO_MLP><<<pgrid, kPThreads, smem, s>>>(P);
     }
     return;
   }

@@ -99,6 +99,7 @@ struct lopt_plan {
   int64_t max_mn = 0;        // max over tensors of m + n
   int64_t factor_sums = 0;   // f64 entries of the all-reducible factor block
   int64_t n_tiles = 0;       // fast path: 128-element tiles
+  int64_t n_pairs = 0;       // fast path: tile pairs (pair kernel)
   // workspace regions
   Region r_desc, r_fitems, r_sitems, r_aitems, r_tscal, r_step, r_status, r_maxabs, r_imaxabs,
       r_abort, r_fsums, r_rowpart, r_colpart, r_rowtab, r_coltab, r_statpart, r_sumsq, r_weights,
@@ -274,6 +275,10 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
       }
       d.tiles = (int32_t)tiles;
       p->n_tiles += tiles;
+      d.pair0 = p->n_pairs;
+      d.pairs = (int32_t)(d.rowblock ? (int64_t)((d.m_rows + 1) / 2) * (t.n / apply_chunk)
+                                     : (tiles + 1) / 2);
+      p->n_pairs += d.pairs;
     } else {
       for (int64_t e = t.lo; e < t.hi; e += apply_chunk)
         p->aitems.push_back(ChunkItem{j, 0, e, std::min<int64_t>(t.hi, e + apply_chunk)});
@@ -327,6 +332,7 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   P.alpha = cfg->alpha;
   P.beta_out = cfg->beta_out;
   P.n_tiles = p->n_tiles;
+  P.n_pairs = p->n_pairs;
   if (fast && !fast_supported(P)) {
     delete p;
     return LOPT_ERR_UNSUPPORTED;

@@ -50,7 +50,12 @@ struct TensorDesc {
   // a_lo + q % m_rows, columns [128 * (q / m_rows), +128) (column-block major,
   // so a run of tiles shares its column-table entries); otherwise tile q is
   // the flat elements [lo + 128 q, +128)
-  int32_t rowblock, a_lo, m_rows, pad_;
+  int32_t rowblock, a_lo, m_rows;
+  // pair kernel: tile pairs of this tensor and its first pair in the plan
+  // (rowblock: rows 2r, 2r+1 of one column block; flat: tiles 2q, 2q+1; a
+  // missing second tile is an empty tile)
+  int32_t pairs;
+  int64_t pair0;
 };
 
 // Phase-0 tile: rows [a0, a1) x columns [b0, b1) of one tensor.
@@ -108,6 +113,7 @@ struct DevicePlan {
   float alpha, beta_out;
   // fast path
   int64_t n_tiles;        // 128-element tiles over all tensors
+  int64_t n_pairs;        // tile pairs over all tensors (pair kernel)
   unsigned char *prep;    // per-tensor PrepImage (B operands, layer-3 weights)
   double *bcsum;          // [count x d_feat] closed-form sums of broadcast features
   int32_t dbg, n_peers;   // dbg: timing experiments only (LOPT_APPLY_DEBUG), 0 in production

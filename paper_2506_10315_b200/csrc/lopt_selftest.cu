@@ -180,6 +180,59 @@ __global__ void __launch_bounds__(128) umma_probe_kernel(int batch, int rounds, 
   if (warp == 0) tc::tmem_dealloc(base, 512);
 }
 
+
+// TMEM load/store throughput probe: `warps` warps (multiple of 4) each run
+// `rounds` iterations of `per` tcgen05.ld (mode 0: x16, 1: x32) or
+// tcgen05.st (mode 2: x16) followed by one wait; out[w] = cycles of warp w.
+__global__ void __launch_bounds__(1024) tmem_probe_kernel(int mode, int per, int rounds, long long *out) {
+  __shared__ uint32_t tbase;
+  const int t = threadIdx.x, warp = t >> 5;
+  if (warp == 0) {
+    tc::tmem_alloc(&tbase, 512);
+    tc::tmem_relinquish();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t col = (uint32_t)(((warp >> 2) * 32) & 511);
+  const uint32_t ta = tbase + lane + col;
+  uint32_t acc = 0;
+  uint32_t r[32];
+  for (int i = 0; i < 32; i++) r[i] = (uint32_t)(t * 7 + i);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int k = 0; k < rounds; k++) {
+    if (mode == 0) {
+      for (int q = 0; q < per; q++) {
+        uint32_t h[16];
+        tc::tmem_ld16(ta + (uint32_t)((q & 1) * 16), h);
+        tc::tmem_ld_wait();
+        acc ^= h[0] ^ h[15];
+      }
+    } else if (mode == 1) {
+      for (int q = 0; q < per; q++) {
+        tc::tmem_ld32(ta, r);
+        tc::tmem_ld_wait();
+        acc ^= r[0] ^ r[31];
+      }
+    } else {
+      for (int q = 0; q < per; q++) {
+        uint32_t h[16];
+        for (int i = 0; i < 16; i++) h[i] = r[i] + (uint32_t)q;
+        tc::tmem_st16(ta + (uint32_t)((q & 1) * 16), h);
+      }
+      tc::tmem_st_wait();
+    }
+  }
+  long long t1 = clock64();
+  if ((t & 31) == 0) out[warp] = t1 - t0;
+  if (acc == 0x12345678u) out[63] = acc;
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tbase, 512);
+}
+
 __global__ void expf_selftest_kernel(const float *x, float *y, int64_t n) {
   __shared__ uint64_t tab[32];
   if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
@@ -206,6 +259,13 @@ extern "C" int lopt_probe_umma(int32_t batch, int32_t rounds, long long *out, vo
   if (N < 16 || N > 256 || N % 16 || issuers > 4) return LOPT_ERR_INVALID;
   lopt::umma_probe_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(b, rounds, N, a_smem, issuers,
                                                                rotate, warp_wide, out);
+  return cudaGetLastError() == cudaSuccess ? LOPT_OK : LOPT_ERR_CUDA;
+}
+
+extern "C" int lopt_probe_tmem(int32_t warps, int32_t mode, int32_t per, int32_t rounds, long long *out,
+                               void *stream) {
+  if (warps < 4 || warps > 32 || warps % 4 || mode < 0 || mode > 2 || per < 1) return LOPT_ERR_INVALID;
+  lopt::tmem_probe_kernel<<<1, 32 * warps, 0, (cudaStream_t)stream>>>(mode, per, rounds, out);
   return cudaGetLastError() == cudaSuccess ? LOPT_OK : LOPT_ERR_CUDA;
 }
 
