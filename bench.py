@@ -232,8 +232,10 @@ def time_device(opt, params, grads, steps, warmup, world):
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
+    h0 = time.perf_counter()
     for _ in range(steps):
         opt.step(**kw)
+    host_ms = (time.perf_counter() - h0) * 1e3 / steps   # enqueue cost (no sync inside)
     end.record()
     torch.cuda.synchronize()
     barrier(world)
@@ -268,6 +270,7 @@ def time_device(opt, params, grads, steps, warmup, world):
         phases["_no_exchange_ms"] = max_over_ranks(s0.elapsed_time(s1), world) / steps
     q = lambda f: per_step[min(len(per_step) - 1, int(f * (len(per_step) - 1) + 0.5))]  # noqa: E731
     phases["_step_quantiles"] = [q(0.1), q(0.5), q(0.9)]
+    phases["_host_ms"] = host_ms
     launches = sum(pl.launches_last_step() for pl in opt.plans())
     return max_over_ranks(ms, world), phases, launches
 
@@ -347,32 +350,26 @@ def time_e2e(opt, params, grads, steps, warmup, world):
     return max_over_ranks(start.elapsed_time(end), world), h2d, d2h
 
 
-def cpu_sample(workload, budget_params):
-    """Largest-first subset of the workload's tensors (2-D views), up to a
-    parameter budget, for the bounded CPU measurement."""
-    from paper_2506_10315_b200 import view_2d
-    from paper_2506_10315_b200.workloads import WORKLOADS
-
-    shapes = [view_2d(s) for _, s in WORKLOADS[workload]()]
-    chosen, total = [], 0
-    # keep the workload's mix: walk the list in order, skip what overflows
-    for s in shapes:
-        n = s[0] * s[1]
-        if total + n <= budget_params:
-            chosen.append(s)
-            total += n
-    return chosen, total
+_INPUTS = {}
 
 
 def run_cpu_oracle(workload, feature_set, budget_params, steps, warmup, threads=0):
+    """The oracle port on a bounded prefix of the workload (census order),
+    with the GPU arm's synthetic inputs (_ref_inputs)."""
     from oracle import oracle as O
 
     kind = O.KIND_BY_NAME[feature_set]
-    shapes, total = cpu_sample(workload, budget_params)
-    rng = np.random.default_rng(0)
-    params = [(rng.standard_normal(s) * 0.02).astype(np.float32) for s in shapes]
-    grads = [(rng.standard_normal(s) * 1e-3).astype(np.float32) for s in shapes]
-    states = [O.OState.zeros(*s) for s in shapes]
+    if workload not in _INPUTS:
+        _INPUTS[workload] = _ref_inputs(workload)
+    P0, G0 = _INPUTS[workload]
+    idx, total = [], 0
+    for j, p in enumerate(P0):   # keep the workload's mix: walk in order, skip what overflows
+        if total + p.size <= budget_params:
+            idx.append(j)
+            total += p.size
+    params = [P0[j].copy() for j in idx]
+    grads = [G0[j] for j in idx]
+    states = [O.OState.zeros(*p.shape) for p in params]
     w = O.random_weights(39 if kind == O.SMALL_FC_LOPT else 29, seed=0)
     for _ in range(warmup):
         O.opt_step(params, states, grads, w, kind, 1.0, threads=threads)
@@ -382,44 +379,210 @@ def run_cpu_oracle(workload, feature_set, budget_params, steps, warmup, threads=
         O.opt_step(params, states, grads, w, kind, 1.0, threads=threads)
         times.append(time.perf_counter() - t0)
     cores = threads if threads > 0 else len(os.sched_getaffinity(0))
-    return {"params": total, "tensors": len(shapes), "step_s": statistics.median(times),
+    return {"params": total, "tensors": len(idx), "step_s": statistics.median(times),
             "cores": cores, "steps": steps}
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def shipped_reference_available():
+    """The unmodified reference package installed into baseline/_ref (pip
+    --target)."""
+    return os.path.isdir(os.path.join(REF_DIR, "lopt"))
+
+
+def _ref_inputs(workload, seed=0):
+    """The GPU arm's synthetic inputs (make_model, same generator and seed) as
+    2-D NumPy arrays -- identical bytes on both arms."""
+    from paper_2506_10315_b200 import view_2d
+
+    params, grads = make_model(workload, "cpu", seed=seed)
+    P = [p.detach().numpy().reshape(view_2d(p.shape)) for p in params]
+    G = [g.numpy().reshape(view_2d(g.shape)) for g in grads]
+    return P, G
+
+
+def _ref_handle(lo, P, idx, feature_set):
+    w = lo.engine.random_weights(39 if feature_set == "small_fc_lopt" else 29, seed=0)
+    spec = (lo.features.small_fc_lopt_spec() if feature_set == "small_fc_lopt"
+            else lo.features.velo_mlp_spec())
+    return lo.optim.OptimizerHandle.fresh([(f"t{j}", P[j].copy()) for j in idx], w, spec)
+
+
+def _ref_proc(conn, idx, feature_set):
+    """Pool worker: the unmodified reference opt_step on its whole tensors."""
+    import lopt as lo
+    import lopt.engine  # noqa: F401
+    import lopt.features  # noqa: F401
+    import lopt.optim  # noqa: F401
+
+    h = _ref_handle(lo, _REF_P, idx, feature_set)
+    g = [_REF_G[j] for j in idx]
+    while conn.recv():
+        t0 = time.perf_counter()
+        lo.optim.opt_step(h, g)
+        conn.send(time.perf_counter() - t0)
+
+
+_REF_P = _REF_G = None
+
+
+def run_shipped_reference(workload, feature_set, steps, warmup, time_budget_s=120.0):
+    """the shipped reference's opt_step (numba, fused
+    path, lr 1) on the GPU arm's inputs -- (ii) all host cores: P forked
+    processes each stepping a disjoint whole-tensor subset (greedy largest
+    first, distsim.py:109-118); tensors are independent, so the results are
+    those of one opt_step -- and (i) one process on one core.  The per-step
+    sample is the largest-first prefix of the census that keeps the whole
+    --steps/--warmup run inside `time_budget_s`."""
+    import multiprocessing as mp
+
+    global _REF_P, _REF_G
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    import lopt as lo
+    import lopt.engine  # noqa: F401
+    import lopt.features  # noqa: F401
+    import lopt.optim  # noqa: F401
+
+    if workload not in _INPUTS:
+        _INPUTS[workload] = _ref_inputs(workload)
+    P, G = _INPUTS[workload]
+    # JIT-compile in the parent so the forked workers inherit the machine code
+    hw = _ref_handle(lo, [P[0][:2, :16].copy(), P[1][:8].copy()], [0, 1], feature_set)
+    lo.optim.opt_step(hw, [G[0][:2, :16].copy(), G[1][:8].copy()])
+    # (i) one process: the largest-first prefix up to ~3 M params, one step
+    sizes = [p.size for p in P]
+    one, tot = [], 0
+    for j in sorted(range(len(P)), key=lambda j: -sizes[j]):
+        if tot + sizes[j] <= 3_000_000:
+            one.append(j)
+            tot += sizes[j]
+    h1 = _ref_handle(lo, P, one, feature_set)
+    t0 = time.perf_counter()
+    lo.optim.opt_step(h1, [G[j] for j in one])
+    t_one = time.perf_counter() - t0
+    rate1 = tot / t_one
+    del h1
+    # (ii) all cores
+    cores = len(os.sched_getaffinity(0))
+    est_rate = rate1 * cores * 0.8
+    budget = time_budget_s / (steps + warmup) * est_rate
+    chosen, total = [], 0
+    for j in sorted(range(len(P)), key=lambda j: -sizes[j]):
+        if total + sizes[j] <= max(budget, sizes[j] if not chosen else 0):
+            chosen.append(j)
+            total += sizes[j]
+    loads = [[0, []] for _ in range(cores)]
+    for j in chosen:                       # greedy largest-first (distsim.make_plan)
+        b = min(loads, key=lambda x: x[0])
+        b[0] += sizes[j]
+        b[1].append(j)
+    _REF_P, _REF_G = P, G
+    ctx = mp.get_context("fork")
+    pipes, procs = [], []
+    for _, idx in loads:
+        if not idx:
+            continue
+        a, b = ctx.Pipe()
+        pr = ctx.Process(target=_ref_proc, args=(b, idx, feature_set), daemon=True)
+        pr.start()
+        pipes.append(a)
+        procs.append(pr)
+    times = []
+    try:
+        for k in range(warmup + steps):
+            t0 = time.perf_counter()
+            for a in pipes:
+                a.send(True)
+            for a in pipes:
+                a.recv()
+            if k >= warmup:
+                times.append(time.perf_counter() - t0)
+    finally:
+        for a in pipes:
+            a.send(False)
+        for pr in procs:
+            pr.join(timeout=10)
+    return {"params": total, "tensors": len(chosen), "step_s": statistics.median(times),
+            "cores": len(procs), "single": {"params": tot, "tensors": len(one), "step_s": t_one}}
+
+
+def cpu_reference(args, n_params, steps, warmup, time_budget_s=120.0):
+    """The CPU baseline of both arms: the shipped reference (baseline/_ref,
+    numba opt_step, all host cores as a process pool) when installed, with the
+    oracle port (oracle/, OpenMP over tensors) timed beside it; else the port
+    alone.  Returns (value Gparams/s, ms per step, cpu_baseline dict)."""
+    if shipped_reference_available() and not os.environ.get("LOPT_REF_PORT"):
+        r = run_shipped_reference(args.workload, args.feature_set, steps, warmup, time_budget_s)
+        value = r["params"] / r["step_s"] / 1e9
+        s1 = r["single"]
+        rp = run_cpu_oracle(args.workload, args.feature_set, n_params, 1, 1)
+        base = {"value": value, "unit": "Gparams/s", "cores": r["cores"], "kind": "reference",
+                "sample": (f"{r['tensors']} of the {args.workload} tensors / {r['params']} params "
+                           f"(largest-first prefix within the time budget), the shipped "
+                           f"reference (baseline/_ref lopt.optim.opt_step, path='fused', numba) "
+                           f"in {r['cores']} forked processes over disjoint whole-tensor "
+                           f"subsets (greedy largest-first), median of {steps} steps"),
+                "single_process": {"value": s1["params"] / s1["step_s"] / 1e9,
+                                   "unit": "Gparams/s", "cores": 1,
+                                   "sample": f"{s1['tensors']} largest tensors / {s1['params']} "
+                                             f"params, one opt_step"},
+                "port": {"value": rp["params"] / rp["step_s"] / 1e9, "unit": "Gparams/s",
+                         "cores": rp["cores"], "kind": "port",
+                         "sample": "the whole workload, oracle/ (bitwise restatement, 64-lane "
+                                   "blocked MLP like engine.py:441-480, OpenMP over tensors), "
+                                   "one step"}}
+        return value, r["step_s"] * 1e3, base
+    budget = int(max(1_000_000, min(args.cpu_budget or n_params, n_params * 40 // (steps + 1))))
+    r = run_cpu_oracle(args.workload, args.feature_set, budget, steps, warmup)
+    value = r["params"] / r["step_s"] / 1e9
+    base = {"value": value, "unit": "Gparams/s", "cores": r["cores"], "kind": "port",
+            "sample": (f"{r['tensors']} of the {args.workload} tensors, {r['params']} params "
+                       f"(largest-first prefix of the census), oracle/ (bitwise restatement of "
+                       f"the reference, OpenMP over tensors), median of {r['steps']} steps")}
+    r1 = run_cpu_oracle(args.workload, args.feature_set, 3_000_000, 1, 0, threads=1)
+    base["single_process"] = {"value": r1["params"] / r1["step_s"] / 1e9, "unit": "Gparams/s",
+                              "cores": 1, "sample": f"{r1['tensors']} tensors / {r1['params']} "
+                                                    f"params, one step"}
+    return value, r["step_s"] * 1e3, base
+
+
 def reference_arm(args, world, rank):
-    """--impl reference: the reference algorithm on the host cores (the oracle
-    port of the reference, all cores), same metric and workload."""
+    """--impl reference: the reference on the host cores (cpu_reference), same
+    metric, config and synthetic inputs as the GPU arm; rank 0 only."""
     if rank != 0:
         return
-    from oracle import oracle as O
-
-    O.lib()
-    # size each step's sample so the whole --steps run stays around two minutes
-    # (~1.5 Mparams/s on 16 host cores): at most --cpu-budget params per step
     from paper_2506_10315_b200.workloads import census
 
-    full = census(args.workload)[1]
-    # the whole workload per step (~3 s on 16 host cores for ViT-B/16), shrunk
-    # only if --steps would push the run past ~2 minutes
-    cap = args.cpu_budget or full
-    budget = int(max(1_000_000, min(cap, full * 40 // (args.steps + 1))))
-    r = run_cpu_oracle(args.workload, args.feature_set, budget, args.steps, 1)
-    value = r["params"] / r["step_s"] / 1e9
-    sample = (f"{r['tensors']} of the {args.workload} tensors, {r['params']} params "
-              f"(largest-first prefix of the census), median of {r['steps']} steps")
+    n_tensors, n_params = census(args.workload)
+    hp = workload_hparams(args.workload)
+    value, ms, base = cpu_reference(args, n_params, args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": metric_name(args), "value": value, "unit": "Gparams/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": r["step_s"] * 1e3, "higher_is_better": True, "scaling": "none",
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "none",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.workload, "feature_set": args.feature_set,
-                   "sample_params": r["params"]},
-        "cpu_baseline": {"value": value, "unit": "Gparams/s", "cores": r["cores"],
-                         "kind": "port", "sample": sample},
+        "config": bench_config(args, hp, n_tensors, n_params, world),
+        "cpu_baseline": base,
         "e2e": {"value": value, "unit": "Gparams/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def bench_config(args, hp, n_tensors, n_params, world):
+    """The workload description shared by both arms (same keys and values)."""
+    return {"workload": args.workload, "feature_set": args.feature_set,
+            "hparams": ({k: (repr(v) if k == "schedule" else v) for k, v in hp.items()}
+                        or {"lr": 1.0, "weight_decay": 0.0}),
+            "tensors": n_tensors, "params": n_params,
+            "parallelism": (("element-sharded" if args.strategy == "range" else
+                             "tensor-owner-sharded") + f" x{world}") if world > 1 else "single",
+            "l2": f"inputs larger than L2 (each f32 array {n_params * 4 / 1e6:.0f} MB > 126 MB)"}
 
 
 METRIC = "optimizer step ms + Gparams/s at ViT-B/16 (small_fc_lopt, VeLO) vs roofline"
@@ -476,6 +639,7 @@ def main():
     achieved = ALGO_BYTES_PER_PARAM * local_params / (apply_ms / 1e3) / 1e9
     quant = phases.pop("_step_quantiles", None)
     no_exchange_ms = phases.pop("_no_exchange_ms", None)
+    host_ms = phases.pop("_host_ms", None)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": None, "kernel": "apply (phase 2)",
                 "peak_source": peak_kind, "frac_vs_8tbs_spec": achieved / 8000.0,
@@ -528,6 +692,7 @@ def main():
                 "ms_per_step": vms / args.steps,
                 "step_ms_p10_p50_p90": vph.pop("_step_quantiles", None),
                 "ms_per_step_without_param_exchange": vph.pop("_no_exchange_ms", None),
+                "host_ms_per_step": vph.pop("_host_ms", None),
                 "phase_ms": {k: statistics.mean(v) for k, v in vph.items()}}
 
     # context: the same parameters stepped by torch's fused
@@ -558,22 +723,25 @@ def main():
         adam["torch_adafactor_foreach_ms_per_step"] = timed_ms(aopt)
         del aopt, params, grads
 
+    # configs 1/2 (BASELINE.json): the 2-layer MNIST MLP, launch-bound -- one
+    # captured-graph launch per step
+    small = None
+    if world == 1 and not args.no_velo and args.workload == "vit_b16":
+        small = {}
+        for fs in ("small_fc_lopt", "velo"):
+            sp, sg = make_model("mnist_mlp", dev, seed=0)
+            so = build_optimizer(sp, fs, args.mode, 1, "range", {})
+            sms, sph, sl = time_device(so, sp, sg, 200, 10, 1)
+            small[fs] = {"ms_per_step": sms / 200, "host_ms_per_step": sph.get("_host_ms"),
+                         "params": 101770, "value": 101770 / (sms / 200 / 1e3) / 1e9,
+                         "unit": "Gparams/s", "kernels_per_step": sl,
+                         "graph_launches_per_step": 1 if so.use_graph else 0}
+            del so, sp, sg
+
     cpu = None
     if not args.no_cpu and world == 1:
-        r = run_cpu_oracle(args.workload, args.feature_set, args.cpu_budget or n_params, 3, 1)
-        cpu = {"value": r["params"] / r["step_s"] / 1e9, "unit": "Gparams/s", "cores": r["cores"],
-               "kind": "port",
-               "sample": f"{r['tensors']} {args.workload} tensors / {r['params']} params, "
-                         f"oracle/ (bitwise restatement of the reference, 64-lane blocked MLP "
-                         f"like engine.py:441-480, OpenMP over tensors), median of 3 steps",
-               "ms_per_step_sample": r["step_s"] * 1e3}
-        # the shipped reference is single-threaded (numba,
-        # no parallel=True); the same port on one core, largest tensors first
-        r1 = run_cpu_oracle(args.workload, args.feature_set, 3_000_000, 1, 0, threads=1)
-        cpu["single_core"] = {"value": r1["params"] / r1["step_s"] / 1e9, "unit": "Gparams/s",
-                              "cores": 1, "sample": f"{r1['tensors']} {args.workload} tensors "
-                                                    f"(largest-first subset up to 3 M params) / "
-                                                    f"{r1['params']} params, one step"}
+        # bounded: three timed steps (plus one warm-up) of the CPU reference
+        cpu = cpu_reference(args, n_params, 3, 1, time_budget_s=30.0)[2]
 
     if rank == 0:
         line = {
@@ -582,19 +750,13 @@ def main():
             "ms_per_step": ms / args.steps, "higher_is_better": True,
             "step_ms_p10_p50_p90": quant,
             "ms_per_step_without_param_exchange": no_exchange_ms,
+            "host_ms_per_step": host_ms,
             "scaling": "strong" if world > 1 else "none", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": args.workload, "feature_set": args.feature_set,
-                       "hparams": ({k: (repr(v) if k == "schedule" else v) for k, v in hp.items()}
-                                   or {"lr": 1.0, "weight_decay": 0.0}),
-                       "mode": args.mode, "tensors": n_tensors, "params": n_params,
-                       "parallelism": (("element-sharded" if args.strategy == "range" else
-                                        "tensor-owner-sharded") + f" x{world}, param exchange "
-                                       f"{gather_used}") if world > 1 else "single",
-                       "l2": f"inputs larger than L2 (each f32 array {n_params * 4 / 1e6:.0f} MB "
-                             f"> 126 MB)"},
+            "mode": args.mode, "param_exchange": gather_used if world > 1 else None,
+            "config": bench_config(args, hp, n_tensors, n_params, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "velo": velo,
-            "context": adam,
+            "context": adam, "mnist_mlp": small,
             "clocks": clocks, "gpu_launches": launches * args.steps,
         }
         print(json.dumps(line), flush=True)

@@ -98,6 +98,10 @@ typedef struct lopt_step_args {
   double weight_decay;
   float time_features[11];
   int32_t t;              /* post-increment step counter */
+  /* VeLO hypernetwork loss inputs {log(loss), EMA of log(loss)} (build-defined,
+   * no reference counterpart); read by the hypernetwork when it was registered
+   * (lopt_set_velo / lopt_velo_mix) with loss_feats == NULL, else ignored. */
+  float loss_features[2];
 } lopt_step_args;
 
 typedef struct lopt_plan lopt_plan;

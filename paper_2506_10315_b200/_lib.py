@@ -74,6 +74,7 @@ class lopt_step_args(ctypes.Structure):
     _fields_ = [
         ("lr", ctypes.c_double), ("weight_decay", ctypes.c_double),
         ("time_features", ctypes.c_float * 11), ("t", ctypes.c_int32),
+        ("loss_features", ctypes.c_float * 2),
     ]
 
 

@@ -479,6 +479,8 @@ static StepScalars make_scalars(const lopt_plan *p, const lopt_step_args *a) {
   h.decay = (float)(1.0 - a->lr * a->weight_decay);             // optim.py:100
   h.apply_decay = a->weight_decay > 0.0 ? 1 : 0;                // optim.py:171
   h.t = a->t;
+  h.loss[0] = a->loss_features[0];
+  h.loss[1] = a->loss_features[1];
   return h;
 }
 
@@ -628,7 +630,8 @@ int lopt_set_velo(lopt_plan *p, const float *hyper, float *lstm_state, const flo
     p->velo = false;
     return LOPT_OK;
   }
-  if (!lstm_state || !bank || !loss_feats || hidden < 1 || hidden > 64 || bank_size < 1 ||
+  // loss_feats == NULL: the loss features come with the step scalars
+  if (!lstm_state || !bank || hidden < 1 || hidden > 64 || bank_size < 1 ||
       bank_size > 16 || p->cfg.feature_set != LOPT_VELO_MLP)
     return LOPT_ERR_INVALID;
   if (p->cfg.num_weight_sets != (int32_t)p->tensors.size()) return LOPT_ERR_INVALID;
@@ -692,7 +695,7 @@ int lopt_debug_ptrs(lopt_plan *p, double **sumsq, float **factor_means) {
 int lopt_velo_mix(lopt_plan *p, const float *hyper, float *lstm_state, const float *bank,
                   const float *loss_feats, int32_t hidden, int32_t bank_size, float *mix_out,
                   void *stream) {
-  if (!p || !p->ws || !hyper || !lstm_state || !bank || !loss_feats) return LOPT_ERR_INVALID;
+  if (!p || !p->ws || !hyper || !lstm_state || !bank) return LOPT_ERR_INVALID;
   if (p->cfg.num_weight_sets != (int32_t)p->tensors.size()) return LOPT_ERR_INVALID;
   for (size_t j = 0; j < p->tensors.size(); j++)
     if (p->tensors[j].weight_slot != (int32_t)j) return LOPT_ERR_INVALID;

@@ -82,7 +82,7 @@ struct StepScalars {
   float decay;            // f32(1 - lr * weight_decay)    (optim.py:100)
   int32_t apply_decay;    // weight_decay > 0               (optim.py:171)
   int32_t t;
-  float pad_[2];
+  float loss[2];          // VeLO hypernetwork loss features (lopt_step_args.loss_features)
 };
 
 // Per-tensor device scalars produced on the device during the step.

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) velo_mix_kernel(DevicePlan P, const float
   const int tid = threadIdx.x;
   if (tid < D) x[tid] = (float)log(T.sumsq[tid] / count + kEpsNorm);
   if (tid < kTimeFeatures) x[29 + tid] = P.step->tf[tid];
-  if (tid < 2) x[40 + tid] = loss_feats[tid];
+  if (tid < 2) x[40 + tid] = loss_feats ? loss_feats[tid] : P.step->loss[tid];
   float *st = lstm_state + (int64_t)j * 2 * H;
   if (tid < H) {
     h[tid] = st[tid];

@@ -133,6 +133,8 @@ class StepPlan:
         self.graph_steps = 0
         self._tf_t = None
         self._velo_key = None
+        # object with .loss_features (the owning optimizer), or None
+        self.loss_src = None
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -192,6 +194,11 @@ class StepPlan:
                 args.time_features[k] = float(tf[k])
             self._tf_t = t
         args.t = int(t)
+        # VeLO's loss features travel with the step scalars (no upload)
+        src = self.loss_src
+        lf = src.loss_features if src is not None else (0.0, 0.0)
+        args.loss_features[0] = lf[0]
+        args.loss_features[1] = lf[1]
         return args
 
     def step(self, lr: float, weight_decay: float, t: int):
@@ -215,11 +222,12 @@ class StepPlan:
             _lib.check(self.L.lopt_set_velo(self.h, None, None, None, None, 0, 0, None))
             self._velo_key = None
             return
+        lp = loss.data_ptr() if loss is not None else None   # None: from the step scalars
         _lib.check(self.L.lopt_set_velo(self.h, hyper.data_ptr(), lstm.data_ptr(),
-                                        bank.data_ptr(), loss.data_ptr(), int(hidden),
+                                        bank.data_ptr(), lp, int(hidden),
                                         int(bank_size), mix.data_ptr() if mix is not None else None),
                    "set_velo")
-        self._velo_key = (hyper.data_ptr(), lstm.data_ptr(), bank.data_ptr(), loss.data_ptr(),
+        self._velo_key = (hyper.data_ptr(), lstm.data_ptr(), bank.data_ptr(), lp,
                           mix.data_ptr() if mix is not None else None)
 
     def set_peers(self, deltas):

@@ -171,6 +171,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
         ptrs = [(s.theta.data_ptr(), s.grad.data_ptr()) for s in slots]
         if cached is None or cached[0] != key:
             plan = StepPlan(slots, self.spec, weights, mode=self.mode)
+            plan.loss_src = self
             if getattr(self, "_peer_deltas", None):
                 plan.set_peers(self._peer_deltas)
         else:
@@ -204,6 +205,10 @@ class LearnedOptimizer(torch.optim.Optimizer):
             self.check()   # raises before the counter moves, like opt_step
         self.T += 1
         return loss
+
+    # VeLO hypernetwork loss inputs (log loss, EMA), passed with the step
+    # scalars of every plan (lopt_step_args.loss_features); unused otherwise
+    loss_features = (0.0, 0.0)
 
     # Hook run after the feature statistics are final and before phase 2
     # (VeLO's hypernetwork mixes the per-tensor MLPs there); None = no hook.
@@ -390,6 +395,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
             ptrs = [(sl.theta.data_ptr(), sl.grad.data_ptr()) for sl in slots]
             if plan is None:
                 plan = StepPlan(slots, self.spec, weights, mode=self.mode)
+                plan.loss_src = self
                 hs["plans"][b][gi] = plan
                 hs["ptrs"][b][gi] = ptrs
             elif hs["ptrs"][b][gi] != ptrs:

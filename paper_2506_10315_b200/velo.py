@@ -68,7 +68,6 @@ class _VeLOMixin:
         dev = self.param_groups[0]["params"][0].device
         self._hyper_dev = torch.from_numpy(self.hypernet.hyper).to(dev)
         self._bank_dev = torch.from_numpy(self.hypernet.packed_bank()).to(dev)
-        self._loss_dev = torch.zeros(2, dtype=torch.float32, device=dev)
         self._loss_ema = None
         self._lstm = {}
 
@@ -114,19 +113,9 @@ class _VeLOMixin:
         # optim.py:160-165) also leaves the loss EMA where it was (check())
         self._loss_ema_prev = self._loss_ema
         self._loss_ema = lv if self._loss_ema is None else 0.9 * self._loss_ema + 0.1 * lv
-        # stream-ordered upload from a small ring of pinned buffers (a pageable
-        # copy would stall the host on every step)
-        ring = getattr(self, "_loss_ring", None)
-        if ring is None:
-            ring = self._loss_ring = [(torch.empty(2, dtype=torch.float32).pin_memory(),
-                                       torch.cuda.Event()) for _ in range(4)]
-            self._loss_k = 0
-        buf, ev = ring[self._loss_k % len(ring)]
-        self._loss_k += 1
-        ev.synchronize()   # the copy that last used this buffer has finished
-        buf[0], buf[1] = lv, self._loss_ema
-        self._loss_dev.copy_(buf, non_blocking=True)
-        ev.record()
+        # the hypernetwork reads them from the step scalars (lopt_step_args):
+        # no upload, nothing to synchronize
+        self.loss_features = (lv, self._loss_ema)
 
     def check(self):
         """LearnedOptimizer.check; an aborted step (OptimError: non-finite
@@ -145,9 +134,9 @@ class _VeLOMixin:
         st = self._lstm_state(gi, params)
         mix = getattr(self, "_mix_out", None)
         key = (self._hyper_dev.data_ptr(), st.data_ptr(), self._bank_dev.data_ptr(),
-               self._loss_dev.data_ptr(), mix.data_ptr() if mix is not None else None)
+               None, mix.data_ptr() if mix is not None else None)
         if plan._velo_key != key:
-            plan.set_velo(self._hyper_dev, st, self._bank_dev, self._loss_dev, self.hypernet.H,
+            plan.set_velo(self._hyper_dev, st, self._bank_dev, None, self.hypernet.H,
                           self.hypernet.K, mix)
         return True
 
@@ -156,7 +145,7 @@ class _VeLOMixin:
         mix = getattr(self, "_mix_out", None)
         _lib.check(plan.L.lopt_velo_mix(
             plan.h, self._hyper_dev.data_ptr(), st.data_ptr(), self._bank_dev.data_ptr(),
-            self._loss_dev.data_ptr(), self.hypernet.H, self.hypernet.K,
+            None, self.hypernet.H, self.hypernet.K,
             mix.data_ptr() if mix is not None else None,
             torch.cuda.current_stream().cuda_stream), "velo_mix")
 
