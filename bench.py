@@ -721,7 +721,40 @@ def main():
         # features build on (torch's foreach Adafactor)
         aopt = torch.optim.Adafactor(params, lr=1e-2, foreach=True)
         adam["torch_adafactor_foreach_ms_per_step"] = timed_ms(aopt)
-        del aopt, params, grads
+        del aopt
+        # the reference's own baselines (optim.py:187-217, same conventions),
+        # restated on the device (paper_2506_10315_b200.baselines), per tensor
+        from paper_2506_10315_b200 import view_2d
+        from paper_2506_10315_b200.baselines import adafactor_step, adam_step
+
+        th2 = [p.detach().view(view_2d(p.shape)) for p in params]
+        gr2 = [g.view(view_2d(g.shape)) for g in grads]
+        ms_ = [torch.zeros_like(t) for t in th2]
+        vs_ = [torch.zeros_like(t) for t in th2]
+        rs_ = [torch.zeros(t.shape[0], device=dev) for t in th2]
+        cs_ = [torch.zeros(t.shape[1], device=dev) for t in th2]
+
+        class _Fn:
+            def __init__(self, f):
+                self.step = f
+
+        k_ = [0]
+
+        def adam_all():
+            k_[0] += 1
+            for t, g, m, v in zip(th2, gr2, ms_, vs_):
+                adam_step(t, g, m, v, lr=1e-3, t=k_[0])
+
+        def afac_all():
+            for t, g, r, c in zip(th2, gr2, rs_, cs_):
+                adafactor_step(t, g, r, c, lr=1e-3)
+
+        adam["reference_adam_step_ms_per_step"] = timed_ms(_Fn(adam_all))
+        adam["reference_adafactor_step_ms_per_step"] = timed_ms(_Fn(afac_all))
+        adam["reference_baselines"] = ("lopt_adam_step / lopt_adafactor_step: the reference's "
+                                       "adam_step / adafactor_step (optim.py:187-217) on the "
+                                       "device, one call per tensor")
+        del params, grads, th2, gr2, ms_, vs_, rs_, cs_
 
     # configs 1/2 (BASELINE.json): the 2-layer MNIST MLP, launch-bound -- one
     # captured-graph launch per step

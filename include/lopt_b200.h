@@ -181,6 +181,21 @@ int lopt_selftest_expf(const float *x, float *y, int64_t n, void *stream);
 /* Micro-benchmark of the fast path's MMA shape: `batch` MMAs per commit,
  * `rounds` commit/wait round trips; out[0] = SM cycles per round. */
 int lopt_probe_umma(int32_t batch, int32_t rounds, long long *out, void *stream);
+/* ---- the reference's hand-designed baselines ----
+ * adam_step, optim.py:187-198: theta, m, v (n f32 each) updated in place.
+ * `scalars` (HOST pointer, 8 f32): {f32(b1), f32(1)-f32(b1), f32(b2), f32(1)-f32(b2),
+ * f32(1)-f32(b1)**f32(t), f32(1)-f32(b2)**f32(t), f32(lr), f32(eps)} -- the
+ * reference's numpy f32 scalars; every element op is the reference's, in order. */
+int lopt_adam_step(float *theta, const float *g, float *m, float *v, int64_t n,
+                   const float *scalars, void *stream);
+/* adafactor_step, optim.py:201-217 (update_adafactor state.py:93-113,
+ * adafactor_scale features.py:357-362): theta (rows x cols), r (rows), c (cols)
+ * updated in place.  `scalars` (HOST pointer, 4 f32): {f32(beta),
+ * f32(1)-f32(beta), f32(lr), f32(eps)}; `scratch`: device memory of
+ * lopt_adafactor_scratch_bytes(rows, cols) bytes (8-byte aligned). */
+int lopt_adafactor_step(float *theta, const float *g, float *r, float *c, int64_t rows,
+                        int64_t cols, const float *scalars, void *scratch, void *stream);
+int64_t lopt_adafactor_scratch_bytes(int64_t rows, int64_t cols);
 /* TMEM ld/st throughput probe (development tool, no reference counterpart). */
 int lopt_probe_tmem(int32_t warps, int32_t mode, int32_t per, int32_t rounds, long long *out, void *stream);
 

@@ -17,6 +17,8 @@ The functions mirror the reference API (paths relative to the reference repo):
     opt_step            pkg/src/lopt/optim.py:144-180 (multi-tensor, OpenMP)
     random_weights      pkg/src/lopt/engine.py:178-192
     schedule_lr         pkg/src/lopt/optim.py:69-89
+    adam_step           pkg/src/lopt/optim.py:187-198  (numpy, f32 op by op)
+    adafactor_step      pkg/src/lopt/optim.py:201-217  (numpy, f32 op by op)
 
 Parity of this oracle with the reference is pinned by tests/test_oracle_golden.py
 against fixtures generated from the reference itself (tests/golden/).
@@ -367,3 +369,50 @@ def view_2d(shape):
     for s in shape[1:]:
         rest *= s
     return (shape[0], rest)
+
+
+# ---------------------------------------------------------------------------
+# The reference's baseline optimizers, restated with
+# explicit f32 scalars: every array op below is one correctly rounded f32
+# operation, in the reference's order.
+
+def adam_step(theta, g, m, v, beta1=0.9, beta2=0.999, lr=1e-3, eps=1e-8, t=1):
+    """pkg/src/lopt/optim.py:187-198.  Returns (theta', m', v')."""
+    if t < 1:
+        raise ValueError("Adam step count starts at 1")
+    one = F32(1.0)
+    b1, b2 = F32(beta1), F32(beta2)
+    th, gr = np.asarray(theta, F32), np.asarray(g, F32)
+    m_new = np.add(np.multiply(b1, m, dtype=F32), np.multiply(one - b1, gr, dtype=F32), dtype=F32)
+    g2 = np.multiply(gr, gr, dtype=F32)
+    v_new = np.add(np.multiply(b2, v, dtype=F32), np.multiply(one - b2, g2, dtype=F32), dtype=F32)
+    c1 = one - b1 ** F32(t)   # numpy's f32 *scalar* power, as the reference (the
+    c2 = one - b2 ** F32(t)   # array ufunc path can round differently)
+    mh = np.divide(m_new, c1, dtype=F32)
+    vh = np.divide(v_new, c2, dtype=F32)
+    den = np.add(np.sqrt(vh, dtype=F32), F32(eps), dtype=F32)
+    step = np.divide(np.multiply(F32(lr), mh, dtype=F32), den, dtype=F32)
+    return np.subtract(th, step, dtype=F32), m_new, v_new
+
+
+def adafactor_step(theta, g, r, c, beta=0.999, lr=1e-3, eps=1e-30):
+    """pkg/src/lopt/optim.py:201-217 with update_adafactor (state.py:93-113)
+    and adafactor_scale (features.py:357-362).  Returns (theta', r', c')."""
+    gr = np.asarray(g, F32)
+    rows, cols = gr.shape
+    if rows == 0 or cols == 0:
+        raise ValueError("adafactor factors undefined for empty tensors")
+    sq = gr.astype(np.float64) ** 2                     # exact: f32 squares fit in f64
+    row_mean = (sq.sum(axis=1) / cols).astype(F32)      # numpy mean = sum / count, f64
+    col_mean = (sq.sum(axis=0) / rows).astype(F32)
+    b = F32(beta)
+    omb = F32(1.0) - b
+    r_new = np.add(np.multiply(b, r, dtype=F32), np.multiply(omb, row_mean, dtype=F32), dtype=F32)
+    c_new = np.add(np.multiply(b, c, dtype=F32), np.multiply(omb, col_mean, dtype=F32), dtype=F32)
+    # np.mean(r, dtype=f64) casts in 8192-element buffers; one buffer (this
+    # form) for rows <= 8192, which covers the golden cases
+    mean_r = F32(r_new.astype(np.float64).sum() / rows)
+    outer = np.multiply(r_new[:, None], c_new[None, :], dtype=F32)
+    S = np.sqrt(np.divide(mean_r, np.add(outer, F32(eps), dtype=F32), dtype=F32), dtype=F32)
+    upd = np.multiply(np.multiply(F32(lr), gr, dtype=F32), S, dtype=F32)
+    return np.subtract(np.asarray(theta, F32), upd, dtype=F32), r_new, c_new

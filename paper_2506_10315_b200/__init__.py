@@ -3,7 +3,8 @@ torch.optim surface, with sm_100a kernels reached through a C ABI
 (include/lopt_b200.h).  See DESIGN.md."""
 
 from .engine import (DeviceOptState, EngineError, FeatureStats, Slot, StepPlan, UpdateOverflowError,
-                     fast_available, fused_apply, fused_stats, step_fused, step_naive)
+                     fast_available, fused_apply, fused_stats, step_fused, step_naive,
+                     UpdateReport)
 from .features import (FeatureSet, FeatureSetSpec, column_names, small_fc_lopt_spec,
                        spec_by_name, time_features, velo_mlp_spec)
 from .optim import AdafacLO_CUDA, LearnedOptimizer, OptimError, view_2d
@@ -16,6 +17,6 @@ __all__ = [
     "fast_available", "FeatureSet", "FeatureSetSpec", "FeatureStats", "fused_apply",
     "fused_stats", "LearnedOptimizer", "LoptWeights", "OptimError", "random_weights",
     "schedule_lr", "ScheduleConfig", "Slot", "small_fc_lopt_spec", "spec_by_name",
-    "step_fused", "step_naive", "StepPlan", "time_features", "UpdateOverflowError",
+    "step_fused", "step_naive", "StepPlan", "time_features", "UpdateOverflowError", "UpdateReport",
     "VeLO_CUDA", "velo_mlp_spec", "VeLOHyperNet", "view_2d", "zero_weights",
 ]

@@ -34,7 +34,8 @@ EXPORTS = [
     "lopt_read_status", "lopt_debug_ptrs", "lopt_version",
     "lopt_num_kernels_launched_last_step", "lopt_velo_mix", "lopt_selftest_umma",
     "lopt_probe_umma", "lopt_selftest_expf", "lopt_set_peers", "lopt_graph_step",
-    "lopt_graph_reset", "lopt_set_velo", "lopt_probe_tmem",
+    "lopt_graph_reset", "lopt_set_velo", "lopt_probe_tmem", "lopt_adam_step",
+    "lopt_adafactor_step", "lopt_adafactor_scratch_bytes",
 ]
 
 
@@ -127,6 +128,9 @@ def lib(required: bool = True):
     L.lopt_selftest_umma.argtypes = [i32, i32, vp, vp, vp, vp]
     L.lopt_probe_umma.argtypes = [i32, i32, vp, vp]
     L.lopt_probe_tmem.argtypes = [i32, i32, i32, i32, vp, vp]
+    L.lopt_adam_step.argtypes = [vp, vp, vp, vp, ctypes.c_int64, vp, vp]
+    L.lopt_adafactor_step.argtypes = [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp]
+    L.lopt_adafactor_scratch_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
     L.lopt_set_peers.argtypes = [vp, i32, vp]
     L.lopt_selftest_expf.argtypes = [vp, vp, ctypes.c_int64, vp]
     L.lopt_graph_step.argtypes = [vp, ctypes.POINTER(lopt_step_args), vp]
@@ -136,6 +140,7 @@ def lib(required: bool = True):
         f = getattr(L, name)
         if name != "lopt_version":
             f.restype = ctypes.c_int
+    L.lopt_adafactor_scratch_bytes.restype = ctypes.c_int64
     _lib = L
     return L
 

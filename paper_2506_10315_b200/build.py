@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 SO = os.path.join(LIBDIR, "liblopt_b200.so")
 SOURCES = ["lopt_capi.cu", "lopt_factors.cu", "lopt_strict.cu", "lopt_fast.cu",
-           "lopt_apply_tc.cu", "lopt_velo.cu", "lopt_selftest.cu"]
+           "lopt_apply_tc.cu", "lopt_velo.cu", "lopt_selftest.cu", "lopt_baselines.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

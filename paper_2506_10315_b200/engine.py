@@ -417,20 +417,55 @@ def fused_apply(W, g, state: DeviceOptState, weights: LoptWeights, spec, stats, 
     return float(mx[0])
 
 
+@dataclass
+class UpdateReport:
+    """engine.py:253-262, filled from the device: the pass times are CUDA
+    event intervals on the launching stream (pass 1 = factor finalize +
+    feature statistics, pass 2 = apply), `kernel_equivalents` the kernels the
+    step launched, `scratch_peak_bytes` the plan's device workspace.  Item
+    access (report["max_abs_update"]) is kept for dict-style callers."""
+
+    tensor_name: str
+    elements: int
+    max_abs_update: float
+    stats_pass_s: float
+    apply_pass_s: float
+    kernel_equivalents: int
+    scratch_peak_bytes: int
+
+    def __getitem__(self, key):
+        if key == "kernel_launches":
+            return self.kernel_equivalents
+        return getattr(self, key)
+
+
 def step_fused(W, g, state: DeviceOptState, weights: LoptWeights, spec=None, lr: float = 1.0,
                workers: int = 1, tracker=None, tensor_name: str = "", mode="strict"):
-    """engine.py:713-748: returns (new W tensor, report dict).  The state must
+    """engine.py:713-748: returns (new W tensor, UpdateReport).  The state must
     already be advanced for g."""
     spec = spec or small_fc_lopt_spec()
     _check_step_inputs(W, g, state, weights, spec)
     out = W.detach().clone().contiguous()
     plan = _engine_plan(out, g.detach(), state, weights, spec, mode)
-    plan.step(lr, 0.0, state.t)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    plan.set_step(lr, 0.0, state.t)
+    plan.factor_partials()
+    ev[0].record()
+    plan.factor_finalize()
+    plan.feature_stats()
+    ev[1].record()
+    plan.apply()
+    ev[2].record()
     st, mx = plan.status()
+    ev[2].synchronize()
     if st[0] & _lib.LOPT_STATUS_NONFINITE_PARAM:
         raise UpdateOverflowError(f"non-finite parameters after fused step {tensor_name!r}")
-    report = {"tensor_name": tensor_name, "elements": W.numel(), "max_abs_update": float(mx[0]),
-              "kernel_launches": plan.launches_last_step()}
+    report = UpdateReport(tensor_name=tensor_name, elements=W.numel(),
+                          max_abs_update=float(mx[0]),
+                          stats_pass_s=ev[0].elapsed_time(ev[1]) / 1e3,
+                          apply_pass_s=ev[1].elapsed_time(ev[2]) / 1e3,
+                          kernel_equivalents=plan.launches_last_step(),
+                          scratch_peak_bytes=plan.ws_bytes)
     return out, report
 
 

@@ -192,3 +192,36 @@ def test_view_rule():
     assert view_2d((1, 1, 768)) == (1, 768)
     assert view_2d((1, 197, 768)) == (197, 768)
     assert view_2d((768, 3, 16, 16)) == (768, 768)
+
+
+BASE = load_golden("baseline_cases.npz")
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_adam_oracle_bitwise(oracle, k):
+    """Oracle adam_step == the reference's (optim.py:187-198), 4 chained steps."""
+    th = BASE[f"adam{k}/theta0"]
+    m = np.zeros_like(th)
+    v = np.zeros_like(th)
+    for t in range(1, 5):
+        th, m, v = oracle.adam_step(th, BASE[f"adam{k}/g{t}"], m, v, lr=1e-3 if t != 3 else 0.05, t=t)
+        for nm, got in (("theta", th), ("m", m), ("v", v)):
+            assert np.array_equal(got.view(np.uint32), BASE[f"adam{k}/{nm}{t}"].view(np.uint32)), (nm, t)
+
+
+@pytest.mark.parametrize("k", range(5))
+def test_adafactor_oracle_bitwise(oracle, k):
+    """Oracle adafactor_step == the reference's (optim.py:201-217), 3 chained steps."""
+    th = BASE[f"afac{k}/theta0"]
+    r = np.zeros(th.shape[0], np.float32)
+    c = np.zeros(th.shape[1], np.float32)
+    for t in range(1, 4):
+        th, r, c = oracle.adafactor_step(th, BASE[f"afac{k}/g{t}"], r, c, lr=1e-2 if t == 2 else 1e-3)
+        for nm, got in (("theta", th), ("r", r), ("c", c)):
+            assert np.array_equal(got.view(np.uint32), BASE[f"afac{k}/{nm}{t}"].view(np.uint32)), (nm, t)
+
+
+def test_adam_oracle_rejects_t0(oracle):
+    with pytest.raises(ValueError):
+        oracle.adam_step(np.zeros(2, np.float32), np.zeros(2, np.float32), np.zeros(2, np.float32),
+                    np.zeros(2, np.float32), t=0)
