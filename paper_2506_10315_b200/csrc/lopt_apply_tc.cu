@@ -794,6 +794,9 @@ struct __align__(1024) PairSmem {
   uint64_t img_full[kImgs];    // producer -> WGs: operand image loaded
   int32_t done[kPWGs][4];      // WG warps: last pair finished (image-buffer reuse)
   uint32_t tmem_base;
+  // fused all-gather: each WG stages its pair's updated theta (double
+  // buffered) for the 16-byte peer stores
+  __align__(16) float peer_stage[kPWGs][2][2][128];
 };
 
 // Walks a CTA's pairs in order (one lane), staging both tiles of each.
@@ -1060,6 +1063,7 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
     int red_j = -1;
     float red_max = 0.0f, red_out = 0.0f;
     Entry ce, ce1;
+    int32_t it = 0;   // this warpgroup's iteration count (peer staging buffer)
     for (int32_t i = wg; i < np; i += kPWGs) {
       const Pos<kPRing> rc(i);
       tc::mbar_wait(&S.full[rc.i], rc.phase);
@@ -1088,6 +1092,7 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
       bool valid[2];
       float w[2];
       float *tp[2];
+      int32_t pv0[2], pv1[2], pfl[2];   // peer stores: valid range and flags per tile
       float4 *sp[2];
       FastIn x[2];
       Entry re[2];
@@ -1109,6 +1114,9 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
         const int32_t fl = k == 0 ? flags0 : flags1;
         valid[k] = row >= mt.v0 && row < mt.v1;
         tp[k] = mt.theta + row;
+        pv0[k] = mt.v0;
+        pv1[k] = mt.v1;
+        pfl[k] = fl;
         float g;
         float4 sq4;
         if (!(fl & kFlagSlow)) {
@@ -1238,19 +1246,49 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
         asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&S.done[wg][warp & 3])),
                      "r"(i)
                      : "memory");
+      float out[2];
 #pragma unroll
       for (int k = 0; k < 2; k++) {
         const float dir = de[k].x + dd[k].x, mag = de[k].y + dd[k].y;
         const float du = dsb * (dir * ex2_ftz(mag * alpha_log2e));   // engine.py:537-539
-        const float out = (w[k] + du) * decay;                       // optim.py:100-101
+        out[k] = (w[k] + du) * decay;                                // optim.py:100-101
         if (valid[k]) {
           red_max = fmaxf(red_max, fabsf(du));
-          red_out = max_nan_abs(red_out, out);
-          *tp[k] = out;
-          for (int q = 0; q < n_peers; q++)
-            *reinterpret_cast<float *>(reinterpret_cast<char *>(tp[k]) + P.peer_delta[q]) = out;
+          red_out = max_nan_abs(red_out, out[k]);
+          *tp[k] = out[k];
         }
       }
+      if (n_peers > 0) {
+        // fused all-gather: the same values into every
+        // peer's copy of the arena over NVLink.  Aligned tiles are staged in
+        // shared memory and leave as 16-byte stores: thread t owns chunk
+        // t % 64 (four elements of one tile) and sends it to peers t / 64,
+        // t / 64 + 2, ... -- one shared load and n_peers / 2 vector stores
+        // per thread instead of n_peers scalar stores per element.
+        // Unaligned tiles store element by element.
+        if (P.peer_bulk && !((pfl[0] | pfl[1]) & kFlagSlow)) {
+          const int b = it & 1;   // double buffer: reused two pairs later,
+                                  // past this pair's MMA barriers
+          S.peer_stage[wg][b][0][row] = out[0];
+          S.peer_stage[wg][b][1][row] = out[1];
+          tc::bar_sync(4 + wg, 128);
+          const int c = row & 63, kk = c >> 5, e = (c & 31) * 4;
+          const int32_t lo_ = kk ? pv0[1] : pv0[0], hi_ = kk ? pv1[1] : pv1[0];
+          if (e >= lo_ && e + 4 <= hi_) {
+            const float4 v4 = *reinterpret_cast<const float4 *>(&S.peer_stage[wg][b][kk][e]);
+            char *dst = reinterpret_cast<char *>((kk ? tp[1] : tp[0]) - row + e);
+            for (int q = row >> 6; q < n_peers; q += 2)
+              *reinterpret_cast<float4 *>(dst + P.peer_delta[q]) = v4;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 2; k++)
+            if (valid[k])
+              for (int q = 0; q < n_peers; q++)
+                *reinterpret_cast<float *>(reinterpret_cast<char *>(tp[k]) + P.peer_delta[q]) = out[k];
+        }
+      }
+      it++;
     }
     if (red_j >= 0) {
       if (red_max > 0.0f)

@@ -710,6 +710,10 @@ int lopt_set_peers(lopt_plan *p, int32_t count, const int64_t *deltas) {
   if (count > 0 && p->cfg.mode != LOPT_MODE_FAST) return LOPT_ERR_UNSUPPORTED;
   p->dp.n_peers = count;
   for (int k = 0; k < LOPT_MAX_PEERS; k++) p->dp.peer_delta[k] = k < count ? deltas[k] : 0;
+  p->dp.peer_bulk = 1;
+  for (int k = 0; k < count; k++)
+    if (deltas[k] % 16 != 0) p->dp.peer_bulk = 0;
+  if (getenv("LOPT_PEER_SCALAR")) p->dp.peer_bulk = 0;   // A/B of the element-wise path
   p->drop_graph();   // the plan is captured by value
   return LOPT_OK;
 }

@@ -117,6 +117,7 @@ struct DevicePlan {
   unsigned char *prep;    // per-tensor PrepImage (B operands, layer-3 weights)
   double *bcsum;          // [count x d_feat] closed-form sums of broadcast features
   int32_t dbg, n_peers;   // dbg: timing experiments only (LOPT_APPLY_DEBUG), 0 in production
+  int32_t peer_bulk, pad_peer;   // every peer delta is 16-byte aligned: vector peer stores allowed
   int64_t peer_delta[LOPT_MAX_PEERS];   // fused all-gather: byte offsets of the peer copies
 };
 

@@ -352,3 +352,42 @@ def test_step_host_accepts_numpy_arrays(P):
     torch.cuda.synchronize()
     for p, h in zip(a, out):
         assert p.detach().cpu().numpy().tobytes() == h.tobytes()
+
+
+@pytest.mark.parametrize("n_peers", [1, 7])
+def test_fused_peer_bulk_copies_model_shapes(P, n_peers):
+    """Bulk (TMA) peer copies of whole tiles: ViT-like aligned shapes with
+    many tiles per CTA (both staging buffers cycle), up to LOPT_MAX_PEERS
+    stand-in peers; every peer arena must equal the stepped local arena."""
+    import torch
+
+    shapes = [(768, 768), (2304,), (768, 3072), (197, 768), (1000,), (5, 7)]
+    total = sum(int(np.prod(s)) for s in shapes)
+    rng = np.random.default_rng(11)
+    arena = torch.zeros(total, device="cuda")
+    ps, off = [], 0
+    for s in shapes:
+        n = int(np.prod(s))
+        arena[off:off + n].copy_(torch.from_numpy(np.asarray(rng.standard_normal(n) * 0.02, F32)))
+        ps.append(torch.nn.Parameter(arena[off:off + n].view(s)))
+        off += n
+    ref = arena.clone()
+    peers = [torch.full((total,), -3.0, device="cuda") for _ in range(n_peers)]
+    opt = P.LearnedOptimizer(ps, mode="fast")
+    opt.set_peer_copies([q.data_ptr() - arena.data_ptr() for q in peers])
+    rps, off = [], 0
+    for s in shapes:
+        n = int(np.prod(s))
+        rps.append(torch.nn.Parameter(ref[off:off + n].view(s)))
+        off += n
+    ropt = P.LearnedOptimizer(rps, mode="fast")
+    for step in range(2):
+        for p, q in zip(ps, rps):
+            g = torch.from_numpy(np.asarray(rng.standard_normal(p.shape) * 1e-3, F32)).cuda()
+            p.grad, q.grad = g, g.clone()
+        opt.step()
+        ropt.step()
+    torch.cuda.synchronize()
+    assert torch.equal(arena, ref)
+    for q in peers:
+        assert torch.equal(q, arena)
