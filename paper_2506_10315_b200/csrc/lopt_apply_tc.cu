@@ -310,7 +310,10 @@ __device__ __forceinline__ void issue_layer1_nc(uint64_t dimg, uint32_t op, uint
   issue_layer1<false>(dimg, op, acc, nullptr);
 }
 
-template <bool kCommit = true>
+// H operand column layout: kHInter = false: [hi K0-15 | hi K16-31 | lo K0-15 |
+// lo K16-31] (8 columns each); true: [hi K0-15 | lo K0-15 | hi K16-31 | lo
+// K16-31], so each 16-unit half of the layer-1 epilogue is one 16-column store.
+template <bool kCommit = true, bool kHInter = false>
 __device__ __forceinline__ void issue_layer2(uint64_t dimg, uint32_t op, uint32_t acc,
                                              uint32_t one, uint64_t *bar) {
   constexpr uint32_t idesc = tc::idesc_f16_f32(128, kN2);
@@ -319,17 +322,18 @@ __device__ __forceinline__ void issue_layer2(uint64_t dimg, uint32_t op, uint32_
   const uint64_t l0 = dimg + slice_off(offsetof(PrepImage, b2[2]));
   const uint64_t l1 = dimg + slice_off(offsetof(PrepImage, b2[3]));
   const uint64_t bb = dimg + slice_off(offsetof(PrepImage, b2[4]));
-  tc::mma_ts(acc, op + 0, h0, idesc, 0);
-  tc::mma_ts(acc, op + 8, h1, idesc, 1);
-  tc::mma_ts(acc, op + 16, h0, idesc, 1);
-  tc::mma_ts(acc, op + 24, h1, idesc, 1);
-  tc::mma_ts(acc, op + 0, l0, idesc, 1);
-  tc::mma_ts(acc, op + 8, l1, idesc, 1);
+  constexpr uint32_t kHi0 = 0, kHi1 = kHInter ? 16 : 8, kLo0 = kHInter ? 8 : 16, kLo1 = 24;
+  tc::mma_ts(acc, op + kHi0, h0, idesc, 0);
+  tc::mma_ts(acc, op + kHi1, h1, idesc, 1);
+  tc::mma_ts(acc, op + kLo0, h0, idesc, 1);
+  tc::mma_ts(acc, op + kLo1, h1, idesc, 1);
+  tc::mma_ts(acc, op + kHi0, l0, idesc, 1);
+  tc::mma_ts(acc, op + kHi1, l1, idesc, 1);
   tc::mma_ts(acc, one, bb, idesc, 1);
   if (kCommit) tc::mma_commit(bar);
 }
 __device__ __forceinline__ void issue_layer2_nc(uint64_t dimg, uint32_t op, uint32_t acc, uint32_t one) {
-  issue_layer2<false>(dimg, op, acc, one, nullptr);
+  issue_layer2<false, true>(dimg, op, acc, one, nullptr);
 }
 
 __device__ __forceinline__ float ex2_ftz(float x) {
@@ -1091,8 +1095,6 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
       // ---- inputs of both tiles
       bool valid[2];
       float w[2];
-      float *tp[2];
-      int32_t pv0[2], pv1[2], pfl[2];   // peer stores: valid range and flags per tile
       float4 *sp[2];
       FastIn x[2];
       Entry re[2];
@@ -1113,10 +1115,6 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
         const TileMeta &mt = st.meta[k];
         const int32_t fl = k == 0 ? flags0 : flags1;
         valid[k] = row >= mt.v0 && row < mt.v1;
-        tp[k] = mt.theta + row;
-        pv0[k] = mt.v0;
-        pv1[k] = mt.v1;
-        pfl[k] = fl;
         float g;
         float4 sq4;
         if (!(fl & kFlagSlow)) {
@@ -1179,16 +1177,14 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
         tc::tmem_ld16(ta0 + 32 + 16 * half, h0);
         tc::tmem_ld16(ta1 + 32 + 16 * half, h1);
         tc::tmem_ld_wait();
-        uint32_t hi0[8], lo0[8], hi1[8], lo1[8];
+        uint32_t o0[16], o1[16];   // {hi(8) | lo(8)} of this 16-unit half
 #pragma unroll
         for (int q = 0; q < 8; q++) {
-          relu_split2(__uint_as_float(h0[2 * q]), __uint_as_float(h0[2 * q + 1]), hi0[q], lo0[q]);
-          relu_split2(__uint_as_float(h1[2 * q]), __uint_as_float(h1[2 * q + 1]), hi1[q], lo1[q]);
+          relu_split2(__uint_as_float(h0[2 * q]), __uint_as_float(h0[2 * q + 1]), o0[q], o0[8 + q]);
+          relu_split2(__uint_as_float(h1[2 * q]), __uint_as_float(h1[2 * q + 1]), o1[q], o1[8 + q]);
         }
-        tc::tmem_st8(ta0 + 8 * half, hi0);
-        tc::tmem_st8(ta0 + 16 + 8 * half, lo0);
-        tc::tmem_st8(ta1 + 8 * half, hi1);
-        tc::tmem_st8(ta1 + 16 + 8 * half, lo1);
+        tc::tmem_st16(ta0 + 16 * half, o0);
+        tc::tmem_st16(ta1 + 16 * half, o1);
       }
       tc::tmem_st_wait();
       tc::fence_before_sync();
@@ -1197,7 +1193,7 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
         tc::fence_after_sync();
         if (tc::elect_one()) {
           issue_layer2_nc(dimg2 + doff, op0, op0 + 32, one);
-          issue_layer2(dimg2 + doff, op1, op1 + 32, one, &S.acc[wg]);
+          issue_layer2<true, true>(dimg2 + doff, op1, op1 + 32, one, &S.acc[wg]);
         }
         __syncwarp();
       } else {
@@ -1239,23 +1235,28 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
           }
         }
       }
-      // the data slot and (for the producer's image reuse) this pair are done
-      mbar_arrive(&S.data_free[rc.i]);
-      __syncwarp();   // every lane's image reads precede lane 0's release
-      if ((flags0 & kFlagTail) && (threadIdx.x & 31) == 0)
-        asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&S.done[wg][warp & 3])),
-                     "r"(i)
-                     : "memory");
+      // ---- update and stores; the tile metadata and theta are re-read from
+      // the data slot (not held in registers across the MMA waits)
       float out[2];
+      float *tpk[2];
+      bool vk[2];
+      int32_t kv0[2], kv1[2], kfl[2];
 #pragma unroll
       for (int k = 0; k < 2; k++) {
+        const TileMeta &mt = st.meta[k];
+        kv0[k] = mt.v0;
+        kv1[k] = mt.v1;
+        kfl[k] = mt.flags;
+        vk[k] = row >= kv0[k] && row < kv1[k];
+        tpk[k] = mt.theta + row;
+        const float wk = !(kfl[k] & kFlagSlow) ? st.th[k][row] : (vk[k] ? *tpk[k] : 0.0f);
         const float dir = de[k].x + dd[k].x, mag = de[k].y + dd[k].y;
         const float du = dsb * (dir * ex2_ftz(mag * alpha_log2e));   // engine.py:537-539
-        out[k] = (w[k] + du) * decay;                                // optim.py:100-101
-        if (valid[k]) {
+        out[k] = (wk + du) * decay;                                  // optim.py:100-101
+        if (vk[k]) {
           red_max = fmaxf(red_max, fabsf(du));
           red_out = max_nan_abs(red_out, out[k]);
-          *tp[k] = out[k];
+          *tpk[k] = out[k];
         }
       }
       if (n_peers > 0) {
@@ -1266,28 +1267,35 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
         // t / 64 + 2, ... -- one shared load and n_peers / 2 vector stores
         // per thread instead of n_peers scalar stores per element.
         // Unaligned tiles store element by element.
-        if (P.peer_bulk && !((pfl[0] | pfl[1]) & kFlagSlow)) {
+        if (P.peer_bulk && !((kfl[0] | kfl[1]) & kFlagSlow)) {
           const int b = it & 1;   // double buffer: reused two pairs later,
                                   // past this pair's MMA barriers
           S.peer_stage[wg][b][0][row] = out[0];
           S.peer_stage[wg][b][1][row] = out[1];
           tc::bar_sync(4 + wg, 128);
           const int c = row & 63, kk = c >> 5, e = (c & 31) * 4;
-          const int32_t lo_ = kk ? pv0[1] : pv0[0], hi_ = kk ? pv1[1] : pv1[0];
+          const int32_t lo_ = kk ? kv0[1] : kv0[0], hi_ = kk ? kv1[1] : kv1[0];
           if (e >= lo_ && e + 4 <= hi_) {
             const float4 v4 = *reinterpret_cast<const float4 *>(&S.peer_stage[wg][b][kk][e]);
-            char *dst = reinterpret_cast<char *>((kk ? tp[1] : tp[0]) - row + e);
+            char *dst = reinterpret_cast<char *>((kk ? tpk[1] : tpk[0]) - row + e);
             for (int q = row >> 6; q < n_peers; q += 2)
               *reinterpret_cast<float4 *>(dst + P.peer_delta[q]) = v4;
           }
         } else {
 #pragma unroll
           for (int k = 0; k < 2; k++)
-            if (valid[k])
+            if (vk[k])
               for (int q = 0; q < n_peers; q++)
-                *reinterpret_cast<float *>(reinterpret_cast<char *>(tp[k]) + P.peer_delta[q]) = out[k];
+                *reinterpret_cast<float *>(reinterpret_cast<char *>(tpk[k]) + P.peer_delta[q]) = out[k];
         }
       }
+      // the data slot and (for the producer's image reuse) this pair are done
+      mbar_arrive(&S.data_free[rc.i]);
+      __syncwarp();   // every lane's image reads precede lane 0's release
+      if ((flags0 & kFlagTail) && (threadIdx.x & 31) == 0)
+        asm volatile("st.release.cta.shared.b32 [%0], %1;\n" ::"r"(tc::smem_u32(&S.done[wg][warp & 3])),
+                     "r"(i)
+                     : "memory");
       it++;
     }
     if (red_j >= 0) {
