@@ -170,8 +170,10 @@ def test_optimizer_vs_oracle_vit_like_shapes_one_step(P, oracle):
         got = p.detach().cpu().numpy().reshape(-1)
         want = q.reshape(-1)
         bad = np.count_nonzero(got != want)
-        assert bad == 0 or np.all(np.abs(got - want) <= 1e-5 * (1 + np.abs(want))), bad
-        assert bad <= 2, bad
+        # bitwise: the device's f64 reduction orders differ from numpy's, but
+        # on these inputs no f32 rounding of a factor mean, normalization scale
+        # or feature flips
+        assert bad == 0, (q.shape, bad, np.max(np.abs(got - want)))
 
 
 def test_nonfinite_gradient_raises_and_changes_nothing(P):
