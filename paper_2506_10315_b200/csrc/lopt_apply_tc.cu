@@ -918,10 +918,11 @@ struct PairProducer {
   }
 };
 
-// Features of one element -> the tile's E (hi | lo) and B operand words.
+// Features of one element -> the tile's E (hi | lo) operand words, stored to
+// TMEM at `ta`, and the B operand words.
 template <int KIND>
 __device__ __forceinline__ void pair_operands(const FastIn &x, const Entry &re, const Entry &ce,
-                                              const PrepImage &im, uint32_t (&ev)[16],
+                                              const PrepImage &im, uint32_t ta,
                                               uint32_t (&bv)[16]) {
   const float sq[3] = {im.sqmr[0], im.sqmr[1], im.sqmr[2]};
   float f[16];
@@ -935,8 +936,10 @@ __device__ __forceinline__ void pair_operands(const FastIn &x, const Entry &re, 
     const float2 p1 = fmul2(make_float2(f[4 * q + 2], f[4 * q + 3]), make_float2(e4.z, e4.w));
     f[4 * q] = p0.x; f[4 * q + 1] = p0.y; f[4 * q + 2] = p1.x; f[4 * q + 3] = p1.y;
   }
+  uint32_t ev[16];
 #pragma unroll
   for (int q = 0; q < 8; q++) split2(f[2 * q], f[2 * q + 1], ev[q], ev[8 + q]);
+  tc::tmem_st16(ta, ev);
   uint32_t xh = 0, xl = 0;
   if (KIND == LOPT_VELO_MLP) split2(clip01(x.g) * im.escale[16], 0.0f, xh, xl);
   bv[0] = re.hi[0]; bv[1] = re.hi[1]; bv[2] = re.hi[2];
@@ -947,6 +950,64 @@ __device__ __forceinline__ void pair_operands(const FastIn &x, const Entry &re, 
   bv[11] = ce.lo[0]; bv[12] = ce.lo[1]; bv[13] = ce.lo[2];
   bv[14] = xl & 0xFFFFu;
   bv[15] = 0u;
+}
+
+// The producer warps' loop (one elected lane each): walk the CTA's pairs,
+// load each tensor's operand image once its buffer is free, stage the pairs of
+// parity p into the ring.
+__device__ __forceinline__ void pair_producer_loop(const DevicePlan &P, PairSmem &S, int p,
+                                                   int32_t pb, int32_t np) {
+  if (tc::elect_one() && np > 0) {
+    PairProducer pr;
+    pr.seek(P, pb);
+    int k = -1, img = 0, cur_j = -1;
+    uint32_t par_bits = 0;
+    int32_t first[kImgs] = {0, 0, 0, 0};
+    Cursor<kPRing> rc;
+    for (int32_t i = 0; i < np; i++) {
+      if (pr.j != cur_j) {
+        cur_j = pr.j;
+        k++;
+        img = k & (kImgs - 1);
+        const int32_t pf = first[img];
+        const int32_t nf = first[(k + 1) & (kImgs - 1)];
+        first[img] = i;
+        if (k >= kImgs) par_bits ^= 1u << img;
+        if (i % kPProducers == p) {
+          if (k >= kImgs) {
+            // tensor k - kImgs used pairs [pf, nf - 1]: every warp of every
+            // WG must be past its last pair in that range
+            const int32_t last = nf - 1;
+            for (int w = 0; w < kPWGs; w++) {
+              const int32_t need = last - (((last - w) % kPWGs) + kPWGs) % kPWGs;
+              if (need < pf) continue;
+              for (int q = 0; q < 4; q++) {
+                int32_t d;
+                while (true) {
+                  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];\n"
+                               : "=r"(d)
+                               : "r"(tc::smem_u32(&S.done[w][q]))
+                               : "memory");
+                  if (d >= need) break;
+                  __nanosleep(32);
+                }
+              }
+            }
+          }
+          mbar_arrive_tx(&S.img_full[img], (uint32_t)sizeof(PrepImage));
+          bulk_g2s(&S.img[img], reinterpret_cast<const PrepImage *>(P.prep) + pr.j,
+                   (uint32_t)sizeof(PrepImage), &S.img_full[img]);
+        }
+      }
+      if (i % kPProducers == p) {
+        // parked in hardware while the ring is full (no issue slots spent)
+        if (rc.wrapped) tc::mbar_sleep(&S.data_free[rc.i], rc.phase ^ 1u);
+        pr.stage(S.stage[rc.i], &S.full[rc.i], img, (int)((par_bits >> img) & 1u));
+      }
+      pr.advance(P);
+      rc.next();
+    }
+  }
 }
 
 template <int KIND>
@@ -992,59 +1053,7 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
   const int32_t np = aborted ? 0 : pe - pb;
 
   if (warp >= kPWarpProducer) {
-    // -------------------------------------------------------------- producers
-    const int p = warp - kPWarpProducer;
-    if (tc::elect_one() && np > 0) {
-      PairProducer pr;
-      pr.seek(P, pb);
-      int k = -1, img = 0, cur_j = -1;
-      uint32_t par_bits = 0;
-      int32_t first[kImgs] = {0, 0, 0, 0};
-      Cursor<kPRing> rc;
-      for (int32_t i = 0; i < np; i++) {
-        if (pr.j != cur_j) {
-          cur_j = pr.j;
-          k++;
-          img = k & (kImgs - 1);
-          const int32_t pf = first[img];
-          const int32_t nf = first[(k + 1) & (kImgs - 1)];
-          first[img] = i;
-          if (k >= kImgs) par_bits ^= 1u << img;
-          if (i % kPProducers == p) {
-            if (k >= kImgs) {
-              // tensor k - kImgs used pairs [pf, nf - 1]: every warp of every
-              // WG must be past its last pair in that range
-              const int32_t last = nf - 1;
-              for (int w = 0; w < kPWGs; w++) {
-                const int32_t need = last - (((last - w) % kPWGs) + kPWGs) % kPWGs;
-                if (need < pf) continue;
-                for (int q = 0; q < 4; q++) {
-                  int32_t d;
-                  while (true) {
-                    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];\n"
-                                 : "=r"(d)
-                                 : "r"(tc::smem_u32(&S.done[w][q]))
-                                 : "memory");
-                    if (d >= need) break;
-                    __nanosleep(32);
-                  }
-                }
-              }
-            }
-            mbar_arrive_tx(&S.img_full[img], (uint32_t)sizeof(PrepImage));
-            bulk_g2s(&S.img[img], reinterpret_cast<const PrepImage *>(P.prep) + pr.j,
-                     (uint32_t)sizeof(PrepImage), &S.img_full[img]);
-          }
-        }
-        if (i % kPProducers == p) {
-          // parked in hardware while the ring is full (no issue slots spent)
-          if (rc.wrapped) tc::mbar_sleep(&S.data_free[rc.i], rc.phase ^ 1u);
-          pr.stage(S.stage[rc.i], &S.full[rc.i], img, (int)((par_bits >> img) & 1u));
-        }
-        pr.advance(P);
-        rc.next();
-      }
-    }
+    pair_producer_loop(P, S, warp - kPWarpProducer, pb, np);
     __syncwarp();
   } else {
     // ------------------------------------------------------ math warpgroups
@@ -1143,12 +1152,10 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
       }
       // ---- features -> E/B operands of both tiles, layer-1 MMAs
       {
-        uint32_t ev[16], bv[16];
-        pair_operands<KIND>(x[0], re[0], ce, im, ev, bv);
-        tc::tmem_st16(ta0, ev);
+        uint32_t bv[16];
+        pair_operands<KIND>(x[0], re[0], ce, im, ta0, bv);
         tc::tmem_st16(ta0 + 16, bv);
-        pair_operands<KIND>(x[1], re[1], ce1, im, ev, bv);
-        tc::tmem_st16(ta1, ev);
+        pair_operands<KIND>(x[1], re[1], ce1, im, ta1, bv);
         tc::tmem_st16(ta1 + 16, bv);
         tc::tmem_st_wait();
       }
