@@ -123,6 +123,11 @@ int lopt_set_weights(lopt_plan *plan, int32_t slot, const float *packed, int32_t
  * e.g. the VeLO mixing kernel). */
 int lopt_weights_ptr(lopt_plan *plan, int32_t slot, float **dev_ptr);
 int lopt_set_step_args(lopt_plan *plan, const lopt_step_args *args, void *stream);
+/* Element count behind each tensor's feature statistics, used by the apply
+ * pass's normalization 1/sqrt(sumsq/count + eps) (features.py:138-140) --
+ * fused_apply's `stats.count` (engine.py:657-710), which the reference accepts
+ * for a partial range; counts[j] == 0 or counts == NULL: the whole tensor. */
+int lopt_set_stat_counts(lopt_plan *plan, const int64_t *counts, void *stream);
 
 int lopt_factor_partials(lopt_plan *plan, void *stream);
 int lopt_factor_finalize(lopt_plan *plan, void *stream);

@@ -35,7 +35,7 @@ EXPORTS = [
     "lopt_num_kernels_launched_last_step", "lopt_velo_mix", "lopt_selftest_umma",
     "lopt_probe_umma", "lopt_selftest_expf", "lopt_set_peers", "lopt_graph_step",
     "lopt_graph_reset", "lopt_set_velo", "lopt_probe_tmem", "lopt_adam_step",
-    "lopt_adafactor_step", "lopt_adafactor_scratch_bytes",
+    "lopt_adafactor_step", "lopt_adafactor_scratch_bytes", "lopt_set_stat_counts",
 ]
 
 
@@ -131,6 +131,7 @@ def lib(required: bool = True):
     L.lopt_adam_step.argtypes = [vp, vp, vp, vp, ctypes.c_int64, vp, vp]
     L.lopt_adafactor_step.argtypes = [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp]
     L.lopt_adafactor_scratch_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
+    L.lopt_set_stat_counts.argtypes = [vp, vp, vp]
     L.lopt_set_peers.argtypes = [vp, i32, vp]
     L.lopt_selftest_expf.argtypes = [vp, vp, ctypes.c_int64, vp]
     L.lopt_graph_step.argtypes = [vp, ctypes.POINTER(lopt_step_args), vp]

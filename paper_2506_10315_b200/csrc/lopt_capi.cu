@@ -453,6 +453,17 @@ int lopt_rebind_tensors(lopt_plan *p, const lopt_tensor *tensors, int32_t count,
                                     (cudaStream_t)stream));
 }
 
+int lopt_set_stat_counts(lopt_plan *p, const int64_t *counts, void *stream) {
+  if (!p || !p->ws) return LOPT_ERR_INVALID;
+  for (size_t j = 0; j < p->descs.size(); j++) {
+    if (counts && counts[j] < 0) return LOPT_ERR_INVALID;
+  }
+  for (size_t j = 0; j < p->descs.size(); j++) p->descs[j].stat_count = counts ? counts[j] : 0;
+  return check_cuda(cudaMemcpyAsync(p->dp.tensors, p->descs.data(),
+                                    sizeof(TensorDesc) * p->descs.size(), cudaMemcpyHostToDevice,
+                                    (cudaStream_t)stream));
+}
+
 int lopt_set_weights(lopt_plan *p, int32_t slot, const float *packed, int32_t is_device,
                      void *stream) {
   if (!p || !p->ws || !packed) return LOPT_ERR_INVALID;

@@ -56,6 +56,9 @@ struct TensorDesc {
   // missing second tile is an empty tile)
   int32_t pairs;
   int64_t pair0;
+  // element count behind the tensor's feature statistics for the apply
+  // pass's normalization (features.py:138-140); 0 = the whole tensor, m * n
+  int64_t stat_count;
 };
 
 // Phase-0 tile: rows [a0, a1) x columns [b0, b1) of one tensor.

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
   __shared__ float bias1[32];
   __shared__ float bound[32];
   __shared__ float s2s[2];
-  const int64_t count = T.m * T.n;
+  const int64_t count = T.stat_count > 0 ? T.stat_count : T.m * T.n;
   for (int k = threadIdx.x; k < D; k += blockDim.x)
     scale[k] = (float)(1.0 / sqrt(T.sumsq[k] / (double)count + kEpsNorm));
   __syncthreads();

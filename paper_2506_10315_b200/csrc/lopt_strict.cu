@@ -156,7 +156,7 @@ __device__ void load_strict_mlp(const DevicePlan &P, const TensorDesc &T, Strict
               *b3 = w3 + 2 * H2;
   // features.py:138-140 normalization_scale, f64 then f32
   __shared__ float scale[kMaxFeat];
-  const int64_t count = T.m * T.n;
+  const int64_t count = T.stat_count > 0 ? T.stat_count : T.m * T.n;
   for (int k = threadIdx.x; k < D; k += blockDim.x)
     scale[k] = (float)(1.0 / sqrt(T.sumsq[k] / (double)count + kEpsNorm));
   __syncthreads();

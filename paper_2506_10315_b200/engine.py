@@ -230,6 +230,17 @@ class StepPlan:
         self._velo_key = (hyper.data_ptr(), lstm.data_ptr(), bank.data_ptr(), lp,
                           mix.data_ptr() if mix is not None else None)
 
+    def set_stat_counts(self, counts):
+        """Element counts behind each tensor's feature statistics for the
+        apply pass's normalization (None: the whole tensors)."""
+        if counts is None:
+            _lib.check(self.L.lopt_set_stat_counts(self.h, None, _stream_handle()), "set_stat_counts")
+            return
+        arr = np.asarray(counts, dtype=np.int64)
+        _lib.check(self.L.lopt_set_stat_counts(self.h, arr.ctypes.data, _stream_handle()),
+                   "set_stat_counts")
+        torch.cuda.current_stream().synchronize()   # the host array is a temporary
+
     def set_peers(self, deltas):
         """Fused parameter all-gather: the apply pass also stores every updated
         parameter at these byte offsets from its local address (the peers'
@@ -398,11 +409,8 @@ def fused_apply(W, g, state: DeviceOptState, weights: LoptWeights, spec, stats, 
         raise EngineError(f"out must be a contiguous tensor shaped {tuple(W.shape)}")
     sumsq, count = (stats[0], stats[1]) if isinstance(stats, tuple) else (stats.sumsq, stats.count)
     m, n = state.shape
-    if int(count) != m * n:
-        # the device folds 1/sqrt(sumsq/(m*n) + eps) into W1 (lopt_fast.cu /
-        # lopt_strict.cu); merged stats always carry the whole-tensor count
-        raise EngineError(f"stats cover {int(count)} elements; the apply pass needs the "
-                          f"whole tensor's ({m * n}) -- merge the range stats first")
+    if int(count) < 1:
+        raise EngineError(f"stats over {int(count)} elements")
     lo_ = 0 if lo is None else int(lo)
     hi_ = m * n if hi is None else int(hi)
     flat = out.view(-1)
@@ -412,6 +420,9 @@ def fused_apply(W, g, state: DeviceOptState, weights: LoptWeights, spec, stats, 
     plan.factor_partials()
     plan.factor_finalize()
     plan.stat_sums()[0].copy_(torch.as_tensor(sumsq, dtype=torch.float64))
+    # the normalization uses the stats' own element count, as the reference
+    # does (a partial-range count normalizes by that range)
+    plan.set_stat_counts([int(count)])
     plan.apply()
     _, mx = plan.status()
     return float(mx[0])

@@ -332,8 +332,18 @@ def test_range_operator_pair_matches_whole_tensor(P, oracle, spec_name, shape, m
         a_, r_ = out.cpu().numpy().astype(np.float64), ref.cpu().numpy()
         assert (np.abs(a_ - r_) / (1 + np.abs(r_))).max() <= 1e-7
     assert max(mx0, mx1) > 0
-    with pytest.raises(P.EngineError):
-        P.fused_apply(W, g, st, w, spec, a, out, lr=0.3, lo=0, hi=k, mode=mode)
+    # a partial-range count normalizes by that count, as the reference does
+    # (engine.py:657-710 accepts any FeatureStats): against the oracle
+    out2 = torch.full_like(W, float("nan"))
+    P.fused_apply(W, g, st, w, spec, a, out2, lr=0.3, lo=0, hi=k, mode=mode)
+    want, _ = O.fused_apply(G[key + "/W"], G[key + "/g"], s, O.random_weights(spec.d_feat, seed=int(G[key + "/wseed"][0])),
+                            O.KIND_BY_NAME[spec_name], a.sumsq.cpu().numpy(), a.count, lr=0.3, lo=0, hi=k)
+    got = out2.cpu().numpy().reshape(-1)[:k]
+    want = want.reshape(-1)[:k]
+    if mode == "strict":
+        assert got.tobytes() == want.tobytes()
+    else:
+        assert (np.abs(got.astype(np.float64) - want) / (1 + np.abs(want))).max() <= 1e-5
 
 
 def test_torch_lr_scheduler_drives_group_lr(P):
