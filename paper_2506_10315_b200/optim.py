@@ -495,9 +495,11 @@ class AdafacLO_CUDA(LearnedOptimizer):
         super().__init__(params, lr=lr, weight_decay=weight_decay, **kw)
 
 
-def opt_step_reference_order(opt: LearnedOptimizer, grads, loss=None):
-    """Functional helper used by tests: assign grads (list in param order)
-    and step, like opt_step(h, grads, loss) (optim.py:144)."""
+def opt_step(opt: LearnedOptimizer, grads, loss=None):
+    """The reference's functional entry point opt_step(h, grads, loss)
+    (optim.py:144-180) over an optimizer: one gradient per parameter in
+    parameter order (device tensors), the same count / shape errors, then
+    one step."""
     ps = [p for g in opt.param_groups for p in g["params"]]
     if len(grads) != len(ps):
         raise OptimError(f"got {len(grads)} gradients for {len(ps)} tensors")

@@ -372,3 +372,27 @@ def test_torch_lr_scheduler_drives_group_lr(P):
     for p, q in zip(a, b):
         assert p.detach().cpu().numpy().tobytes() == q.detach().cpu().numpy().tobytes()
     assert oa.param_groups[0]["lr"] == 0.8 * 0.25
+
+
+def test_functional_opt_step_matches_step(P):
+    """opt_step(opt, grads, loss) (optim.py:144-180's functional surface):
+    same result as assigning .grad and stepping; count and shape errors."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    shapes = [(16, 9), (9,)]
+    init = [(rng.standard_normal(s) * 0.1).astype(F32) for s in shapes]
+    grads = [torch.from_numpy((rng.standard_normal(s) * 1e-2).astype(F32)).cuda() for s in shapes]
+    a = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    b = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+    oa, ob = P.LearnedOptimizer(a, mode="strict"), P.LearnedOptimizer(b, mode="strict")
+    P.opt_step(oa, grads)
+    for p, g in zip(b, grads):
+        p.grad = g
+    ob.step()
+    for p, q in zip(a, b):
+        assert torch.equal(p, q)
+    with pytest.raises(P.OptimError):
+        P.opt_step(oa, grads[:1])
+    with pytest.raises(P.OptimError):
+        P.opt_step(oa, [grads[1], grads[0]])
