@@ -756,6 +756,24 @@ def main():
                                        "device, one call per tensor")
         del params, grads, th2, gr2, ms_, vs_, rs_, cs_
 
+    # config 5 (BASELINE.json): GPT-2 medium, VeLO, cosine schedule + weight
+    # decay 0.01, measured in the same run (single GPU; the config's 8-GPU
+    # sharding is the --gpus path)
+    cfg5 = None
+    if world == 1 and not args.no_velo and args.workload == "vit_b16":
+        gp, gg = make_model("gpt2_medium", dev, seed=0)
+        go = build_optimizer(gp, "velo", args.mode, 1, "range", workload_hparams("gpt2_medium"))
+        gms, gph, gl = time_device(go, gp, gg, 10, args.warmup, 1)
+        n5 = sum(p.numel() for p in gp)
+        cfg5 = {"workload": "gpt2_medium", "optimizer": "VeLO_CUDA", "params": n5,
+                "hparams": {k: (repr(v) if k == "schedule" else v)
+                            for k, v in workload_hparams("gpt2_medium").items()},
+                "ms_per_step": gms / 10, "value": n5 / (gms / 10 / 1e3) / 1e9,
+                "unit": "Gparams/s", "kernels_per_step": gl,
+                "phase_ms": {k: statistics.mean(v) for k, v in gph.items() if not k.startswith("_")}}
+        del go, gp, gg
+        torch.cuda.empty_cache()
+
     # configs 1/2 (BASELINE.json): the 2-layer MNIST MLP, launch-bound -- one
     # captured-graph launch per step
     small = None
@@ -789,7 +807,7 @@ def main():
             "mode": args.mode, "param_exchange": gather_used if world > 1 else None,
             "config": bench_config(args, hp, n_tensors, n_params, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "velo": velo,
-            "context": adam, "mnist_mlp": small,
+            "context": adam, "mnist_mlp": small, "gpt2_medium_velo": cfg5,
             "clocks": clocks, "gpu_launches": launches * args.steps,
         }
         print(json.dumps(line), flush=True)
