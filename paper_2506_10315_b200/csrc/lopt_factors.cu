@@ -340,9 +340,10 @@ __global__ void factor_finalize_kernel(DevicePlan P) {
 // broadcast columns over this call's elements [lo, hi): sum_a cnt_a * x(a)^2
 // and sum_b cnt_b * y(b)^2, so phase 1 only has to reduce the per-element
 // columns.
-__global__ void __launch_bounds__(256) factor_means_kernel(DevicePlan P) {
+constexpr int kMeansThreads = 1024;   // the row/column loops are latency-bound
+__global__ void __launch_bounds__(kMeansThreads) factor_means_kernel(DevicePlan P) {
   const TensorDesc T = P.tensors[blockIdx.x];
-  constexpr int NW = 256 / 32;
+  constexpr int NW = kMeansThreads / 32;
   __shared__ double red[15][NW];
   const bool bc = P.bcsum != nullptr;
   double acc[15];
@@ -436,7 +437,7 @@ void launch_factor_finalize(const DevicePlan &P, int64_t max_mn, cudaStream_t s)
 }
 
 void launch_factor_means(const DevicePlan &P, cudaStream_t s) {
-  factor_means_kernel<<<P.count, 256, 0, s>>>(P);
+  factor_means_kernel<<<P.count, kMeansThreads, 0, s>>>(P);
 }
 
 }  // namespace lopt

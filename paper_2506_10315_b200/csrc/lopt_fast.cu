@@ -44,8 +44,9 @@ __device__ __forceinline__ void prep_tab(float *tab, const float *sc) {
 // (features.py:138-140), the layer-1 bias with the time columns folded in,
 // fp16 two-term splits of the weights in the UMMA layout, the layer-2 input
 // exponent s2, and the scaled broadcast-feature operands of every row/column.
+constexpr int kPrepThreads = 1024;   // the row/column table loops are latency-bound
 template <int KIND>
-__global__ void __launch_bounds__(256) prep_kernel(DevicePlan P) {
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(DevicePlan P) {
   constexpr int D = d_feat(KIND);
   const int j = blockIdx.x;
   const TensorDesc T = P.tensors[j];
@@ -357,9 +358,9 @@ void launch_tc_apply(const DevicePlan &P, cudaStream_t s);
 
 void launch_fast_apply(const DevicePlan &P, cudaStream_t s) {
   if (P.kind == LOPT_SMALL_FC_LOPT)
-    prep_kernel<LOPT_SMALL_FC_LOPT><<<P.count, 256, 0, s>>>(P);
+    prep_kernel<LOPT_SMALL_FC_LOPT><<<P.count, kPrepThreads, 0, s>>>(P);
   else
-    prep_kernel<LOPT_VELO_MLP><<<P.count, 256, 0, s>>>(P);
+    prep_kernel<LOPT_VELO_MLP><<<P.count, kPrepThreads, 0, s>>>(P);
   if (P.n_tiles > 0) launch_tc_apply(P, s);
 }
 
