@@ -213,6 +213,10 @@ int lopt_probe_tmem(int32_t warps, int32_t mode, int32_t per, int32_t rounds, lo
  * collective.  count = 0 disables it.  The caller orders the peers' writes
  * before the next use of the parameters (a cross-rank barrier after the step). */
 #define LOPT_MAX_PEERS 7
+/* Enables the current device's kernels to access `peer_device`'s memory
+ * (NVLink peer access), once per pair; LOPT_ERR_UNSUPPORTED without P2P.
+ * The fused exchange calls it for every peer before lopt_set_peers. */
+int lopt_enable_peer_access(int32_t peer_device);
 int lopt_set_peers(lopt_plan *plan, int32_t count, const int64_t *deltas);
 
 const char *lopt_version(void);

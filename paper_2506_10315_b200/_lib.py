@@ -36,6 +36,7 @@ EXPORTS = [
     "lopt_probe_umma", "lopt_selftest_expf", "lopt_set_peers", "lopt_graph_step",
     "lopt_graph_reset", "lopt_set_velo", "lopt_probe_tmem", "lopt_adam_step",
     "lopt_adafactor_step", "lopt_adafactor_scratch_bytes", "lopt_set_stat_counts",
+    "lopt_enable_peer_access",
 ]
 
 
@@ -132,6 +133,7 @@ def lib(required: bool = True):
     L.lopt_adafactor_step.argtypes = [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp]
     L.lopt_adafactor_scratch_bytes.argtypes = [ctypes.c_int64, ctypes.c_int64]
     L.lopt_set_stat_counts.argtypes = [vp, vp, vp]
+    L.lopt_enable_peer_access.argtypes = [i32]
     L.lopt_set_peers.argtypes = [vp, i32, vp]
     L.lopt_selftest_expf.argtypes = [vp, vp, ctypes.c_int64, vp]
     L.lopt_graph_step.argtypes = [vp, ctypes.POINTER(lopt_step_args), vp]

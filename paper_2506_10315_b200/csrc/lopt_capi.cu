@@ -716,6 +716,19 @@ int lopt_velo_mix(lopt_plan *p, const float *hyper, float *lstm_state, const flo
   return st;
 }
 
+int lopt_enable_peer_access(int32_t peer_device) {
+  int cur = 0, can = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return LOPT_ERR_CUDA;
+  if (peer_device == cur) return LOPT_OK;
+  if (cudaDeviceCanAccessPeer(&can, cur, peer_device) != cudaSuccess || !can) return LOPT_ERR_UNSUPPORTED;
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();   // not an error here: clear it
+    return LOPT_OK;
+  }
+  return check_cuda(e);
+}
+
 int lopt_set_peers(lopt_plan *p, int32_t count, const int64_t *deltas) {
   if (!p || count < 0 || count > LOPT_MAX_PEERS || (count > 0 && !deltas)) return LOPT_ERR_INVALID;
   if (count > 0 && p->cfg.mode != LOPT_MODE_FAST) return LOPT_ERR_UNSUPPORTED;

@@ -191,6 +191,16 @@ class ShardedLearnedOptimizer(LearnedOptimizer):
             handles = [None] * self.world
             dist.all_gather_object(handles, reduce_tensor(self.flat), group=self.pg)
             self._peers = [fn(*args) for r, (fn, args) in enumerate(handles) if r != self.rank]
+            # the apply kernel on this device stores into the peers' memory:
+            # peer access from this device to each peer's device, explicitly
+            # (IPC's lazy enable is tied to the context the handle was opened in)
+            from . import _lib
+
+            L = _lib.require_cuda()
+            with torch.cuda.device(dev):
+                for q in self._peers:
+                    if q.device != dev:
+                        _lib.check(L.lopt_enable_peer_access(q.device.index), "enable_peer_access")
             base = self.flat.data_ptr()
             self._peer_offsets = [q.data_ptr() - base for q in self._peers]
             self.set_peer_copies(self._peer_offsets)
