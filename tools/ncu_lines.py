@@ -1,6 +1,7 @@
 """Attribute one ncu capture's executed instructions to CUDA source lines.
 
     python tools/ncu_lines.py <report.ncu-rep> <object.o> <mangled kernel> [elements] [top]
+    (LOPT_NCU_KERNEL=regex selects one kernel of a multi-kernel report)
 
 The SASS page of the report gives executed warp-instructions per address; the
 object's cubin, disassembled with line info (nvdisasm -g), maps each offset to
@@ -21,7 +22,8 @@ rep, obj, fun = sys.argv[1:4]
 elems = float(sys.argv[4]) if len(sys.argv) > 4 else 86567656.0
 top = int(sys.argv[5]) if len(sys.argv) > 5 else 60
 
-src = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'sass'],
+KF = ['-k', 'regex:' + os.environ['LOPT_NCU_KERNEL']] if os.environ.get('LOPT_NCU_KERNEL') else []
+src = subprocess.run(['ncu', '-i', rep] + KF + ['--page', 'source', '--csv', '--print-source', 'sass'],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hdr, data = rows[1], rows[2:]
