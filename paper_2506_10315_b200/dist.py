@@ -492,6 +492,11 @@ def _sharded_velo_cls():
             super().__init__(params, lr=lr, weight_decay=weight_decay, feature_set="velo_mlp",
                              weights=hn.bank[0], **kw)
             self._velo_init(hn)
+            # the loss is a host scalar: averaged over a gloo group on the
+            # host, so a step never waits for the device queue to drain (an
+            # NCCL all-reduce + .item() would block on the previous step)
+            ranks = dist.get_process_group_ranks(self.pg or dist.group.WORLD)
+            self._host_pg = dist.new_group(ranks=ranks, backend="gloo") if self._nccl() else self.pg
 
         def step(self, closure=None, loss=None):
             if closure is not None:
@@ -506,10 +511,10 @@ def _sharded_velo_cls():
             return super().step(loss=loss)
 
         def global_loss(self, loss) -> float:
-            """Mean of `loss` over the ranks of the process group."""
-            dev = self.flat.device if self._nccl() else "cpu"
-            t = torch.tensor([float(loss)], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, group=self.pg)
+            """Mean of `loss` over the ranks of the process group (host
+            all-reduce over gloo)."""
+            t = torch.tensor([float(loss)], dtype=torch.float64)
+            dist.all_reduce(t, group=self._host_pg)
             return float(t.item()) / self.world
 
     return ShardedVeLO
