@@ -171,3 +171,26 @@ def test_optimizer_rejects_host_tensors_before_any_device_call():
     opt = P.LearnedOptimizer([p])
     with pytest.raises(TypeError, match="CUDA"):
         opt.step()
+
+
+def test_fast_mode_size_limit_and_strict_beyond_it():
+    """The tensor-core apply pass indexes a tensor's elements with 32-bit
+    integers: a tensor of 2^31 or more elements is LOPT_ERR_UNSUPPORTED in fast
+    mode (the caller falls back to strict mode, which takes it), never a
+    silent overflow."""
+    from paper_2506_10315_b200 import _lib
+
+    big = _tensor(1 << 16, 1 << 15)          # 2^31 elements
+    assert _create([big], _cfg(mode=1))[0] == _lib.LOPT_ERR_UNSUPPORTED
+    assert _create([_tensor(1 << 16, (1 << 15) - 1)], _cfg(mode=1))[0] == 0
+    rc, nbytes = _create([big], _cfg(mode=0))
+    assert rc == 0 and nbytes > 0
+
+
+def test_fast_plan_odd_row_counts_and_ranges():
+    """Tile pairs: odd row counts (an empty second tile closes each column
+    block) and element-range shards that start and end inside rows plan
+    without error in fast mode."""
+    rc, _ = _create([_tensor(197, 768), _tensor(1, 768), _tensor(3, 128, lo=70, hi=300),
+                     _tensor(1000, 1), _tensor(5, 7)], _cfg(mode=1))
+    assert rc == 0
