@@ -176,8 +176,7 @@ def test_optimizer_rejects_host_tensors_before_any_device_call():
 def test_fast_mode_size_limit_and_strict_beyond_it():
     """The tensor-core apply pass indexes a tensor's elements with 32-bit
     integers: a tensor of 2^31 or more elements is LOPT_ERR_UNSUPPORTED in fast
-    mode (the caller falls back to strict mode, which takes it), never a
-    silent overflow."""
+    mode (a loud error, never a silent overflow); strict mode takes it."""
     from paper_2506_10315_b200 import _lib
 
     big = _tensor(1 << 16, 1 << 15)          # 2^31 elements
