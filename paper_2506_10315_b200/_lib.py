@@ -10,7 +10,8 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(PKG, "_lib", "liblopt_b200.so")
+# LOPT_SO: an alternative build of the same library (tuning experiments only)
+SO = os.environ.get("LOPT_SO") or os.path.join(PKG, "_lib", "liblopt_b200.so")
 
 LOPT_OK = 0
 LOPT_ERR_INVALID = 1

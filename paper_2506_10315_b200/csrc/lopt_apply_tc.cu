@@ -773,9 +773,15 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
 // warpgroup barriers per 256 elements, and two independent elements per thread
 // for ILP between the MMA waits.  Measured against the role-specialized kernel
 // (ncu, ViT-B/16): 396 vs 516 thread-instructions per element, 1.61 vs 1.84 ms.
+#ifndef LOPT_PRING
+#define LOPT_PRING 12   // data-ring depth in pairs (tuning builds override it)
+#endif
+#ifndef LOPT_PPROD
+#define LOPT_PPROD 2    // producer warps
+#endif
 constexpr int kPWGs = 3;
-constexpr int kPRing = 12;
-constexpr int kPProducers = 2;
+constexpr int kPRing = LOPT_PRING;
+constexpr int kPProducers = LOPT_PPROD;
 constexpr int kPThreads = kPWGs * 128 + kPProducers * 32;
 constexpr int kPWarpProducer = kPWGs * 4;
 constexpr uint32_t kPOneCol = 2 * kSlotCols * kPWGs;
