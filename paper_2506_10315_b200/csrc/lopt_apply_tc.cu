@@ -776,8 +776,14 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
 #ifndef LOPT_PRING
 #define LOPT_PRING 12   // data-ring depth in pairs (tuning builds override it)
 #endif
+#ifndef LOPT_ACC_SLEEP
+#define LOPT_ACC_SLEEP 0   // MMA-commit waits parked in hardware (suspend hint)
+#endif
+#ifndef LOPT_STATE_EARLY
+#define LOPT_STATE_EARLY 0 // advanced accumulators stored before the layer-1 issue
+#endif
 #ifndef LOPT_PPROD
-#define LOPT_PPROD 2    // producer warps
+#define LOPT_PPROD 4    // producer warps (2: +4 %, 1: +1 % apply time, same-box ncu A/B)
 #endif
 constexpr int kPWGs = 3;
 constexpr int kPRing = LOPT_PRING;
@@ -1155,6 +1161,9 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
         x[k].w = w[k];
         sp[k] = mt.state + row;
         advance(g, sq4, adv, beta, x[k]);
+#if LOPT_STATE_EARLY
+        if (valid[k] && !adv) *sp[k] = make_float4(x[k].m1, x[k].m2, x[k].m3, x[k].v);
+#endif
       }
       // ---- features -> E/B operands of both tiles, layer-1 MMAs
       {
@@ -1177,11 +1186,17 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
       } else {
         tc::bar_arrive(bar_id, 128);
       }
+#if !LOPT_STATE_EARLY
       // the accumulators do not depend on the MLP: stored while layer 1 runs
 #pragma unroll
       for (int k = 0; k < 2; k++)
         if (valid[k] && !adv) *sp[k] = make_float4(x[k].m1, x[k].m2, x[k].m3, x[k].v);
+#endif
+#if LOPT_ACC_SLEEP
+      tc::mbar_sleep(&S.acc[wg], 0u);
+#else
       tc::mbar_wait(&S.acc[wg], 0u);
+#endif
       tc::fence_after_sync();
       // ---- layer-1 epilogue (ReLU + split -> H) of both tiles, layer-2 MMAs
 #pragma unroll
@@ -1212,7 +1227,11 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
       } else {
         tc::bar_arrive(bar_id, 128);
       }
+#if LOPT_ACC_SLEEP
+      tc::mbar_sleep(&S.acc[wg], 1u);
+#else
       tc::mbar_wait(&S.acc[wg], 1u);
+#endif
       tc::fence_after_sync();
       // ---- layer 3 in f32: (b3 + linear half, from the MMA) + sum (w3/2)|h2|
       float2 de[2], dd[2];

@@ -12,3 +12,4 @@ for v in $VARIANTS; do
   LOPT_SO=/tmp/lopt_$name.so timeout -s KILL 200 python -m pytest tests/test_gpu_fast.py -q -x 2>&1 | tail -1
   run $name /tmp/lopt_$name.so
 done
+run base_again ""
