@@ -782,6 +782,12 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
 #ifndef LOPT_STATE_EARLY
 #define LOPT_STATE_EARLY 0 // advanced accumulators stored before the layer-1 issue
 #endif
+#ifndef LOPT_EPI_PREFETCH
+#define LOPT_EPI_PREFETCH 0   // layer-1 epilogue: both halves' TMEM loads before one wait
+#endif
+#ifndef LOPT_L3_CHAINS8
+#define LOPT_L3_CHAINS8 0   // layer 3: eight FFMA2 chains, all TMEM loads before one wait
+#endif
 #ifndef LOPT_PPROD
 #define LOPT_PPROD 4    // producer warps (2: +4 %, 1: +1 % apply time, same-box ncu A/B)
 #endif
@@ -1199,12 +1205,27 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
 #endif
       tc::fence_after_sync();
       // ---- layer-1 epilogue (ReLU + split -> H) of both tiles, layer-2 MMAs
+#if LOPT_EPI_PREFETCH
+      // all four accumulator loads in flight before the first wait
+      uint32_t hh[2][2][16];
 #pragma unroll
       for (int half = 0; half < 2; half++) {
+        tc::tmem_ld16(ta0 + 32 + 16 * half, hh[half][0]);
+        tc::tmem_ld16(ta1 + 32 + 16 * half, hh[half][1]);
+      }
+      tc::tmem_ld_wait();
+#endif
+#pragma unroll
+      for (int half = 0; half < 2; half++) {
+#if LOPT_EPI_PREFETCH
+        const uint32_t (&h0)[16] = hh[half][0];
+        const uint32_t (&h1)[16] = hh[half][1];
+#else
         uint32_t h0[16], h1[16];
         tc::tmem_ld16(ta0 + 32 + 16 * half, h0);
         tc::tmem_ld16(ta1 + 32 + 16 * half, h1);
         tc::tmem_ld_wait();
+#endif
         uint32_t o0[16], o1[16];   // {hi(8) | lo(8)} of this 16-unit half
 #pragma unroll
         for (int q = 0; q < 8; q++) {
@@ -1233,6 +1254,53 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
       tc::mbar_wait(&S.acc[wg], 1u);
 #endif
       tc::fence_after_sync();
+#if LOPT_L3_CHAINS8
+      // ---- layer 3 in f32: (b3 + linear half, from the MMA) + sum (w3/2)|h2|
+      // as {dir, mag} pairs, eight independent chains (two tiles x two
+      // 16-unit halves x even / odd units), all TMEM loads before one wait
+      float2 de[2], dd[2];
+      {
+        uint32_t h0[16], h1[16], g0[16], g1[16], l0[2], l1[2];
+        tc::tmem_ld16(ta0 + 32, h0);
+        tc::tmem_ld16(ta1 + 32, h1);
+        tc::tmem_ld16(ta0 + 48, g0);
+        tc::tmem_ld16(ta1 + 48, g1);
+        tc::tmem_ld2(ta0 + 64, l0);
+        tc::tmem_ld2(ta1 + 64, l1);
+        tc::tmem_ld_wait();
+        float2 e2[2], d2[2];
+        de[0] = make_float2(__uint_as_float(l0[0]), __uint_as_float(l0[1]));
+        de[1] = make_float2(__uint_as_float(l1[0]), __uint_as_float(l1[1]));
+        dd[0] = dd[1] = e2[0] = e2[1] = d2[0] = d2[1] = make_float2(0.0f, 0.0f);
+        const float4 *w3 = reinterpret_cast<const float4 *>(im.w3h);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const float4 wa = w3[q], wb = w3[8 + q];
+          const float2 wda = make_float2(wa.x, wa.y), wma = make_float2(wa.z, wa.w);
+          const float2 wdb = make_float2(wb.x, wb.y), wmb = make_float2(wb.z, wb.w);
+          float he = fabsf(__uint_as_float(h0[2 * q])), ho = fabsf(__uint_as_float(h0[2 * q + 1]));
+          de[0] = ffma2(make_float2(he, he), wda, de[0]);
+          dd[0] = ffma2(make_float2(ho, ho), wma, dd[0]);
+          he = fabsf(__uint_as_float(h1[2 * q]));
+          ho = fabsf(__uint_as_float(h1[2 * q + 1]));
+          de[1] = ffma2(make_float2(he, he), wda, de[1]);
+          dd[1] = ffma2(make_float2(ho, ho), wma, dd[1]);
+          he = fabsf(__uint_as_float(g0[2 * q]));
+          ho = fabsf(__uint_as_float(g0[2 * q + 1]));
+          e2[0] = ffma2(make_float2(he, he), wdb, e2[0]);
+          d2[0] = ffma2(make_float2(ho, ho), wmb, d2[0]);
+          he = fabsf(__uint_as_float(g1[2 * q]));
+          ho = fabsf(__uint_as_float(g1[2 * q + 1]));
+          e2[1] = ffma2(make_float2(he, he), wdb, e2[1]);
+          d2[1] = ffma2(make_float2(ho, ho), wmb, d2[1]);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+          de[k] = tc::add2(de[k], e2[k]);
+          dd[k] = tc::add2(dd[k], d2[k]);
+        }
+      }
+#else
       // ---- layer 3 in f32: (b3 + linear half, from the MMA) + sum (w3/2)|h2|
       float2 de[2], dd[2];
       {
@@ -1267,6 +1335,7 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
           }
         }
       }
+#endif
       // ---- update and stores; the tile metadata and theta are re-read from
       // the data slot (not held in registers across the MMA waits)
       float out[2];
