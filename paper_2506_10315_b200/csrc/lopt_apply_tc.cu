@@ -788,6 +788,12 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
 #ifndef LOPT_L3_CHAINS8
 #define LOPT_L3_CHAINS8 0   // layer 3: eight FFMA2 chains, all TMEM loads before one wait
 #endif
+#ifndef LOPT_L1_SPLIT
+#define LOPT_L1_SPLIT 0   // tile 0's layer-1 MMAs issued before tile 1's features
+#endif
+#ifndef LOPT_FEAT_ILP
+#define LOPT_FEAT_ILP 0   // both tiles' operands computed before their TMEM stores
+#endif
 #ifndef LOPT_PPROD
 #define LOPT_PPROD 4    // producer warps (2: +4 %, 1: +1 % apply time, same-box ncu A/B)
 #endif
@@ -963,6 +969,36 @@ __device__ __forceinline__ void pair_operands(const FastIn &x, const Entry &re, 
   bv[0] = re.hi[0]; bv[1] = re.hi[1]; bv[2] = re.hi[2];
   bv[3] = ce.hi[0]; bv[4] = ce.hi[1]; bv[5] = ce.hi[2];
   bv[6] = (xh & 0xFFFFu) | 0x3C000000u;   // clip_hi, fp16 1 (bias)
+  bv[7] = 0u;
+  bv[8] = re.lo[0]; bv[9] = re.lo[1]; bv[10] = re.lo[2];
+  bv[11] = ce.lo[0]; bv[12] = ce.lo[1]; bv[13] = ce.lo[2];
+  bv[14] = xl & 0xFFFFu;
+  bv[15] = 0u;
+}
+
+// pair_operands without the store: E words returned in ev (LOPT_FEAT_ILP)
+template <int KIND>
+__device__ __forceinline__ void pair_operands_regs(const FastIn &x, const Entry &re, const Entry &ce,
+                                                   const PrepImage &im, uint32_t (&ev)[16],
+                                                   uint32_t (&bv)[16]) {
+  const float sq[3] = {im.sqmr[0], im.sqmr[1], im.sqmr[2]};
+  float f[16];
+  fast_features(x, re.x, ce.x, sq, f);
+  const float4 *es = reinterpret_cast<const float4 *>(im.escale);
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const float4 e4 = es[q];
+    const float2 p0 = fmul2(make_float2(f[4 * q], f[4 * q + 1]), make_float2(e4.x, e4.y));
+    const float2 p1 = fmul2(make_float2(f[4 * q + 2], f[4 * q + 3]), make_float2(e4.z, e4.w));
+    f[4 * q] = p0.x; f[4 * q + 1] = p0.y; f[4 * q + 2] = p1.x; f[4 * q + 3] = p1.y;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; q++) split2(f[2 * q], f[2 * q + 1], ev[q], ev[8 + q]);
+  uint32_t xh = 0, xl = 0;
+  if (KIND == LOPT_VELO_MLP) split2(clip01(x.g) * im.escale[16], 0.0f, xh, xl);
+  bv[0] = re.hi[0]; bv[1] = re.hi[1]; bv[2] = re.hi[2];
+  bv[3] = ce.hi[0]; bv[4] = ce.hi[1]; bv[5] = ce.hi[2];
+  bv[6] = (xh & 0xFFFFu) | 0x3C000000u;
   bv[7] = 0u;
   bv[8] = re.lo[0]; bv[9] = re.lo[1]; bv[10] = re.lo[2];
   bv[11] = ce.lo[0]; bv[12] = ce.lo[1]; bv[13] = ce.lo[2];
@@ -1172,6 +1208,53 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
 #endif
       }
       // ---- features -> E/B operands of both tiles, layer-1 MMAs
+#if LOPT_L1_SPLIT
+      // tile 0's layer 1 runs while tile 1's features are computed (its own
+      // named barrier: no warp waits on an MMA between the two issues)
+      {
+        uint32_t bv[16];
+        pair_operands<KIND>(x[0], re[0], ce, im, ta0, bv);
+        tc::tmem_st16(ta0 + 16, bv);
+        tc::tmem_st_wait();
+      }
+      tc::fence_before_sync();
+      if (issuer) {
+        tc::bar_sync(7 + wg, 128);
+        tc::fence_after_sync();
+        if (tc::elect_one()) issue_layer1_nc(dimg1 + doff, op0, op0 + 32);
+        __syncwarp();
+      } else {
+        tc::bar_arrive(7 + wg, 128);
+      }
+      {
+        uint32_t bv[16];
+        pair_operands<KIND>(x[1], re[1], ce1, im, ta1, bv);
+        tc::tmem_st16(ta1 + 16, bv);
+        tc::tmem_st_wait();
+      }
+      tc::fence_before_sync();
+      if (issuer) {
+        tc::bar_sync(bar_id, 128);
+        tc::fence_after_sync();
+        if (tc::elect_one()) issue_layer1(dimg1 + doff, op1, op1 + 32, &S.acc[wg]);
+        __syncwarp();
+      } else {
+        tc::bar_arrive(bar_id, 128);
+      }
+#else
+#if LOPT_FEAT_ILP
+      {
+        // both tiles' features computed before any store (interleavable)
+        uint32_t e0[16], b0[16], e1[16], b1[16];
+        pair_operands_regs<KIND>(x[0], re[0], ce, im, e0, b0);
+        pair_operands_regs<KIND>(x[1], re[1], ce1, im, e1, b1);
+        tc::tmem_st16(ta0, e0);
+        tc::tmem_st16(ta0 + 16, b0);
+        tc::tmem_st16(ta1, e1);
+        tc::tmem_st16(ta1 + 16, b1);
+        tc::tmem_st_wait();
+      }
+#else
       {
         uint32_t bv[16];
         pair_operands<KIND>(x[0], re[0], ce, im, ta0, bv);
@@ -1180,6 +1263,7 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
         tc::tmem_st16(ta1 + 16, bv);
         tc::tmem_st_wait();
       }
+#endif
       tc::fence_before_sync();
       if (issuer) {
         tc::bar_sync(bar_id, 128);
@@ -1192,6 +1276,7 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
       } else {
         tc::bar_arrive(bar_id, 128);
       }
+#endif
 #if !LOPT_STATE_EARLY
       // the accumulators do not depend on the MLP: stored while layer 1 runs
 #pragma unroll
