@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(kApplyThreads, 1) apply_tc_kernel(DevicePlan P
 #define LOPT_FEAT_ILP 0   // both tiles' operands computed before their TMEM stores
 #endif
 #ifndef LOPT_PPROD
-#define LOPT_PPROD 4    // producer warps (2: +4 %, 1: +1 % apply time, same-box ncu A/B)
+#define LOPT_PPROD 3    // producer warps, one per math warpgroup (same-box ncu A/B: 4: +0.7 %, 2: +4.5 %)
 #endif
 constexpr int kPWGs = 3;
 constexpr int kPRing = LOPT_PRING;
