@@ -17,8 +17,14 @@
 
 namespace lopt {
 
+#ifndef LOPT_STAT_CHUNK
+#define LOPT_STAT_CHUNK 8192   // elements per stats item (tuning builds override)
+#endif
+#ifndef LOPT_STAT_MINB
+#define LOPT_STAT_MINB 4       // stats CTAs per SM the registers are sized for
+#endif
 constexpr int kFastStatThreads = 256;
-constexpr int64_t kFastStatChunk = 8192;
+constexpr int64_t kFastStatChunk = LOPT_STAT_CHUNK;
 
 __device__ __forceinline__ void split1(float x, uint16_t &hi, uint16_t &lo) {
   uint32_t h, l;
@@ -193,7 +199,7 @@ __device__ __forceinline__ void stats_accum(float w, float g, float4 st, const f
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kFastStatThreads, 4) stats_fast_kernel(DevicePlan P) {
+__global__ void __launch_bounds__(kFastStatThreads, LOPT_STAT_MINB) stats_fast_kernel(DevicePlan P) {
   constexpr int D = d_feat(KIND);
   constexpr int NE = KIND == LOPT_VELO_MLP ? 17 : 16;
   const ChunkItem it = P.stat_items[blockIdx.x];
