@@ -28,6 +28,7 @@ void launch_fast_stats(const DevicePlan &P, cudaStream_t s);
 void launch_fast_apply(const DevicePlan &P, cudaStream_t s);
 int64_t fast_stat_chunk();
 int64_t fast_stat_strip();
+int fast_stat_min_blocks();
 int64_t fast_apply_chunk();
 size_t prep_image_bytes();
 int64_t factor_strip_cols();
@@ -142,6 +143,54 @@ static int check_cuda(cudaError_t e) {
 
 static int check_launch() { return check_cuda(cudaGetLastError()); }
 
+// Fast stats items: the largest chunk (fewest items: each costs a block
+// reduction and a partial-sum write) among 8-32 K elements (32-128 rows of a
+// 256-column strip) whose items are >= 97 % full (rows divide evenly) and
+// still fill >= 6 waves of the stats grid (LOPT_STAT_MINB CTAs x SMs).
+// Same-box ncu sweep on ViT-B/16: 8 K 352 us, 12 K 341, 16 K 337, 20 K 344
+// (partial items), 24 K 330 (the pick), 32 K 343 (4.6 waves).
+static int64_t pick_stat_chunk(const lopt_tensor *tensors, int32_t count) {
+  if (getenv("LOPT_STAT_CHUNK_FIXED")) return fast_stat_chunk();
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+    sms = 148;
+  cudaGetLastError();   // no device (CPU tests): not an error here
+  const int64_t slots = (int64_t)sms * fast_stat_min_blocks();
+  const int64_t strip_w = fast_stat_strip();
+  int64_t best = fast_stat_chunk();
+  for (int64_t c = 8192; c <= 32768; c += 4096) {
+    int64_t items = 0, elems = 0;
+    auto flat = [&](int64_t e0, int64_t e1) {
+      if (e1 > e0) {
+        items += (e1 - e0 + c - 1) / c;
+        elems += e1 - e0;
+      }
+    };
+    for (int j = 0; j < count; j++) {
+      const lopt_tensor &t = tensors[j];
+      if (t.n % strip_w == 0 && t.hi > t.lo) {
+        const int64_t a0 = (t.lo + t.n - 1) / t.n, a1 = t.hi / t.n;
+        if (a1 > a0) {
+          flat(t.lo, a0 * t.n);
+          const int64_t rows = std::max<int64_t>(1, c / strip_w);
+          items += (t.n / strip_w) * ((a1 - a0 + rows - 1) / rows);
+          elems += (a1 - a0) * t.n;
+          flat(a1 * t.n, t.hi);
+        } else {
+          flat(t.lo, t.hi);
+        }
+      } else {
+        flat(t.lo, t.hi);
+      }
+    }
+    if (items == 0) continue;
+    const double fill = (double)elems / ((double)items * (double)c);
+    if (fill >= 0.97 && items >= 6 * slots) best = c;
+  }
+  return best;
+}
+
 extern "C" {
 
 const char *lopt_version(void) { return "lopt_b200 0.1 (sm_100a)"; }
@@ -177,7 +226,7 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   p->descs.resize(count);
   const int D = d_feat(cfg->feature_set);
   const bool fast = cfg->mode == LOPT_MODE_FAST;
-  const int64_t stat_chunk = fast ? fast_stat_chunk() : strict_chunk(0);
+  const int64_t stat_chunk = fast ? pick_stat_chunk(tensors, count) : strict_chunk(0);
   const int64_t apply_chunk = fast ? fast_apply_chunk() : strict_chunk(1);
   int64_t rowpart = 0, colpart = 0, rows = 0, cols = 0;
   for (int j = 0; j < count; j++) {

@@ -341,6 +341,7 @@ int fast_supported(const DevicePlan &P) {
 }
 int64_t fast_stat_chunk() { return kFastStatChunk; }
 int64_t fast_stat_strip() { return kFastStatThreads; }
+int fast_stat_min_blocks() { return LOPT_STAT_MINB; }
 int64_t fast_apply_chunk() { return kTile; }
 size_t prep_image_bytes() { return sizeof(PrepImage); }
 
