@@ -104,7 +104,8 @@ struct lopt_plan {
   // workspace regions
   Region r_desc, r_fitems, r_sitems, r_aitems, r_tscal, r_step, r_status, r_maxabs, r_imaxabs,
       r_abort, r_fsums, r_rowpart, r_colpart, r_rowtab, r_coltab, r_statpart, r_sumsq, r_weights,
-      r_prep, r_bcsum;
+      r_prep, r_bcsum, r_prefix;
+  std::vector<int64_t> prefixes;   // red_prefix (count + 1) then fin_prefix (count + 1)
   size_t ws_bytes = 0;
   char *ws = nullptr;
   DevicePlan dp{};
@@ -364,6 +365,15 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   take(p->r_weights, sizeof(float) * (size_t)wstride * cfg->num_weight_sets);
   take(p->r_prep, fast ? prep_image_bytes() * count : 16);
   take(p->r_bcsum, sizeof(double) * D * count);   // closed-form broadcast sums (both modes)
+  p->prefixes.assign(2 * (size_t)(count + 1), 0);
+  for (int j = 0; j < count; j++) {
+    const lopt_tensor &t = tensors[j];
+    // columns with many row blocks get a warp each, the others a thread
+    const bool wide = p->descs[j].nrowblocks > kWarpColumnBlocks;
+    p->prefixes[j + 1] = p->prefixes[j] + (t.m + 31) / 32 * 32 + (wide ? 32 * t.n : (t.n + 31) / 32 * 32);
+    p->prefixes[count + 1 + j + 1] = p->prefixes[count + 1 + j] + t.m + t.n;
+  }
+  take(p->r_prefix, sizeof(int64_t) * p->prefixes.size());
   p->ws_bytes = align_up(off, 256);
   // device plan (pointers filled at bind time)
   DevicePlan &P = p->dp;
@@ -381,6 +391,8 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   P.alpha = cfg->alpha;
   P.beta_out = cfg->beta_out;
   P.n_tiles = p->n_tiles;
+  P.red_total = p->prefixes[count];
+  P.fin_total = p->prefixes[2 * (size_t)count + 1];
   P.n_pairs = p->n_pairs;
   if (fast && !fast_supported(P)) {
     delete p;
@@ -450,7 +462,13 @@ int lopt_bind_workspace(lopt_plan *p, void *dev_ptr, size_t bytes, void *stream)
   const bool fast = p->cfg.mode == LOPT_MODE_FAST;
   P.prep = fast ? (unsigned char *)(ws + p->r_prep.off) : nullptr;
   P.bcsum = (double *)(ws + p->r_bcsum.off);
+  P.red_prefix = (const int64_t *)(ws + p->r_prefix.off);
+  P.fin_prefix = P.red_prefix + p->descs.size() + 1;
   int st;
+  if ((st = check_cuda(cudaMemcpyAsync(ws + p->r_prefix.off, p->prefixes.data(),
+                                       sizeof(int64_t) * p->prefixes.size(),
+                                       cudaMemcpyHostToDevice, s))))
+    return st;
   if ((st = check_cuda(cudaMemsetAsync(ws + p->r_bcsum.off, 0, p->r_bcsum.bytes, s)))) return st;
   // descriptor uploads: pageable source, so the copies complete before return
   if ((st = check_cuda(cudaMemcpyAsync(P.tensors, p->descs.data(),

@@ -21,6 +21,7 @@ constexpr float kClip = 0.1f;         // features.py:82
 // rsqrt(x7+eps), 0, 0} then, for the fast path, the six values split into bf16
 // hi/lo pairs {hi01, hi23, hi45, 0 | lo01, lo23, lo45, 0}
 constexpr int kRowTab = 16;
+constexpr int kWarpColumnBlocks = 32;   // factor reduce: warp-per-column threshold
 
 __host__ __device__ constexpr int d_feat(int kind) { return kind == LOPT_SMALL_FC_LOPT ? 39 : 29; }
 
@@ -120,7 +121,14 @@ struct DevicePlan {
   unsigned char *prep;    // per-tensor PrepImage (B operands, layer-3 weights)
   double *bcsum;          // [count x d_feat] closed-form sums of broadcast features
   int32_t dbg, n_peers;   // dbg: timing experiments only (LOPT_APPLY_DEBUG), 0 in production
-  int32_t peer_bulk, pad_peer;   // every peer delta is 16-byte aligned: vector peer stores allowed
+  int32_t peer_bulk, pad_peer;
+  // flattened per-tensor work of the factor reduce / finalize kernels: tensor
+  // j owns [red_prefix[j], red_prefix[j + 1]) = roundup(m, 32) rows then one
+  // 32-thread warp per column, and [fin_prefix[j], fin_prefix[j + 1]) = m + n
+  // (columns of tensors with more than kWarpColumnBlocks row blocks take a
+  // warp each in the reduce, the others one thread)
+  const int64_t *red_prefix, *fin_prefix;
+  int64_t red_total, fin_total;   // every peer delta is 16-byte aligned: vector peer stores allowed
   int64_t peer_delta[LOPT_MAX_PEERS];   // fused all-gather: byte offsets of the peer copies
 };
 

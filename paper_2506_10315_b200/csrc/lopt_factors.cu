@@ -276,30 +276,63 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_partials_kernel(Devi
   }
 }
 
-// rowsum[a] = sum over strips of rowpart, colsum[b] = sum over row blocks of
-// colpart, each in a fixed order.  grid: (ceil(max(m+n)/256), count).
-__global__ void factor_reduce_kernel(DevicePlan P) {
-  const TensorDesc T = P.tensors[blockIdx.y];
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < T.m) {
-    double s = 0.0;
-    for (int k = 0; k < T.nstrips; k++) s += T.rowpart[(int64_t)k * T.m + idx];
-    T.rowsum[idx] = s;
-  } else if (idx < T.m + T.n) {
-    const int64_t b = idx - T.m;
-    double s = 0.0;
-    for (int k = 0; k < T.nrowblocks; k++) s += T.colpart[(int64_t)k * T.n + b];
-    T.colsum[b] = s;
+// Tensor owning flattened work index idx: the last j with prefix[j] <= idx.
+__device__ __forceinline__ int tensor_of(const int64_t *prefix, int count, int64_t idx) {
+  int lo = 0, hi = count;   // prefix[lo] <= idx < prefix[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (prefix[mid] <= idx) lo = mid;
+    else hi = mid;
   }
+  return lo;
+}
+
+// rowsum[a] = sum over strips of rowpart, colsum[b] = sum over row blocks of
+// colpart, each in a fixed order.  One flattened grid over every tensor's
+// rows (one thread each, over the <= a few strips) and columns (one warp
+// each: lanes take every 32nd row block, then a fixed shuffle tree -- the
+// GPT-2 embedding has 197 row blocks per column).
+__global__ void factor_reduce_kernel(DevicePlan P) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= P.red_total) return;   // whole warps: every segment is a multiple of 32
+  const int j = tensor_of(P.red_prefix, P.count, idx);
+  const TensorDesc &T = P.tensors[j];
+  const int64_t local = idx - P.red_prefix[j], mpad = (T.m + 31) / 32 * 32;
+  if (local < mpad) {
+    if (local < T.m) {
+      double s = 0.0;
+      for (int k = 0; k < T.nstrips; k++) s += T.rowpart[(int64_t)k * T.m + local];
+      T.rowsum[local] = s;
+    }
+    return;
+  }
+  if (T.nrowblocks <= kWarpColumnBlocks) {   // a thread per column, in order
+    const int64_t b = local - mpad;
+    if (b < T.n) {
+      double s = 0.0;
+      for (int k = 0; k < T.nrowblocks; k++) s += T.colpart[(int64_t)k * T.n + b];
+      T.colsum[b] = s;
+    }
+    return;
+  }
+  const int64_t b = (local - mpad) >> 5;
+  const int lane = (int)(local & 31);
+  double s = 0.0;
+  for (int k = lane; k < T.nrowblocks; k += 32) s += T.colpart[(int64_t)k * T.n + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) T.colsum[b] = s;
 }
 
 // state.py:108-113: mean = f32(sum / len), r' = b*r + (1-b)*mean in f32; then
 // the row/column tables the features read: {x5', x6', x7', 1/sqrt(x'+eps) x3}.
 // With state_advanced the factors are taken as given.
 __global__ void factor_finalize_kernel(DevicePlan P) {
-  const TensorDesc T = P.tensors[blockIdx.y];
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= T.m + T.n) return;
+  const int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gidx >= P.fin_total) return;
+  const int jt = tensor_of(P.fin_prefix, P.count, gidx);
+  const TensorDesc &T = P.tensors[jt];
+  const int64_t idx = gidx - P.fin_prefix[jt];
   const bool is_row = idx < T.m;
   const int64_t i = is_row ? idx : idx - T.m;
   const int64_t len = is_row ? T.m : T.n;
@@ -314,7 +347,7 @@ __global__ void factor_finalize_kernel(DevicePlan P) {
     if (*P.grad_flag != 0.0) {
       // a non-finite gradient on any rank (the flag is all-reduced with the
       // sums): abort before any state is written (optim.py:160-165)
-      if (!isfinite(sum)) atomicOr(&P.status[blockIdx.y], LOPT_STATUS_NONFINITE_GRAD);
+      if (!isfinite(sum)) atomicOr(&P.status[jt], LOPT_STATUS_NONFINITE_GRAD);
       atomicOr(P.abort_flag, 1u);
       return;
     }
@@ -427,13 +460,15 @@ void launch_factor_partials(const DevicePlan &P, cudaStream_t s) {
 }
 
 void launch_factor_reduce(const DevicePlan &P, int64_t max_mn, cudaStream_t s) {
-  dim3 grid((unsigned)((max_mn + 255) / 256), (unsigned)P.count);
-  factor_reduce_kernel<<<grid, 256, 0, s>>>(P);
+  (void)max_mn;
+  if (P.red_total > 0)
+    factor_reduce_kernel<<<(unsigned)((P.red_total + 255) / 256), 256, 0, s>>>(P);
 }
 
 void launch_factor_finalize(const DevicePlan &P, int64_t max_mn, cudaStream_t s) {
-  dim3 grid((unsigned)((max_mn + 255) / 256), (unsigned)P.count);
-  factor_finalize_kernel<<<grid, 256, 0, s>>>(P);
+  (void)max_mn;
+  if (P.fin_total > 0)
+    factor_finalize_kernel<<<(unsigned)((P.fin_total + 255) / 256), 256, 0, s>>>(P);
 }
 
 void launch_factor_means(const DevicePlan &P, cudaStream_t s) {

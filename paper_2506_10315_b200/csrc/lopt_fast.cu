@@ -50,7 +50,8 @@ __device__ __forceinline__ void prep_tab(float *tab, const float *sc) {
 // (features.py:138-140), the layer-1 bias with the time columns folded in,
 // fp16 two-term splits of the weights in the UMMA layout, the layer-2 input
 // exponent s2, and the scaled broadcast-feature operands of every row/column.
-constexpr int kPrepThreads = 1024;   // the row/column table loops are latency-bound
+constexpr int kPrepThreads = 256;
+constexpr int kPrepSplit = 16;   // CTAs per tensor: the row/column table loops are latency-bound
 template <int KIND>
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(DevicePlan P) {
   constexpr int D = d_feat(KIND);
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(DevicePlan P) {
   for (int k = threadIdx.x; k < D; k += blockDim.x)
     scale[k] = (float)(1.0 / sqrt(T.sumsq[k] / (double)count + kEpsNorm));
   __syncthreads();
+  if (blockIdx.y == 0) {
   if (threadIdx.x < 32) {
     const int o = threadIdx.x;
     float b = b1[o];
@@ -162,11 +164,13 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(DevicePlan P) {
     img->s2_down = sd;
     img->pad[0] = img->pad[1] = 0.0f;
   }
+  }   // blockIdx.y == 0
   // broadcast operands: rows r5 r6 r7 rr5 rr6 rr7, columns c5 c6 c7 rc5 rc6 rc7
   const float rs[6] = {scale[4], scale[5], scale[6], scale[14], scale[15], scale[16]};
   const float cs[6] = {scale[7], scale[8], scale[9], scale[17], scale[18], scale[19]};
-  for (int64_t a = threadIdx.x; a < T.m; a += blockDim.x) prep_tab(T.rowtab + a * kRowTab, rs);
-  for (int64_t b = threadIdx.x; b < T.n; b += blockDim.x) prep_tab(T.coltab + b * kRowTab, cs);
+  const int64_t t0 = (int64_t)blockIdx.y * blockDim.x + threadIdx.x, ts = (int64_t)gridDim.y * blockDim.x;
+  for (int64_t a = t0; a < T.m; a += ts) prep_tab(T.rowtab + a * kRowTab, rs);
+  for (int64_t b = t0; b < T.n; b += ts) prep_tab(T.coltab + b * kRowTab, cs);
 }
 
 // Phase 1 (engine.py:619-654): per-element column sums of squares of the 16
@@ -365,9 +369,9 @@ void launch_tc_apply(const DevicePlan &P, cudaStream_t s);
 
 void launch_fast_apply(const DevicePlan &P, cudaStream_t s) {
   if (P.kind == LOPT_SMALL_FC_LOPT)
-    prep_kernel<LOPT_SMALL_FC_LOPT><<<P.count, kPrepThreads, 0, s>>>(P);
+    prep_kernel<LOPT_SMALL_FC_LOPT><<<dim3(P.count, kPrepSplit), kPrepThreads, 0, s>>>(P);
   else
-    prep_kernel<LOPT_VELO_MLP><<<P.count, kPrepThreads, 0, s>>>(P);
+    prep_kernel<LOPT_VELO_MLP><<<dim3(P.count, kPrepSplit), kPrepThreads, 0, s>>>(P);
   if (P.n_tiles > 0) launch_tc_apply(P, s);
 }
 
