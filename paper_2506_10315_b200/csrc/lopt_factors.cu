@@ -17,9 +17,6 @@ namespace lopt {
 constexpr int kFactorThreads = 256;
 constexpr int kFactorWarps = kFactorThreads / 32;
 constexpr int kStripCols = 512;      // columns per tile strip (16 per lane)
-#ifndef LOPT_FACTOR_V2
-#define LOPT_FACTOR_V2 0   // factor partials through factor_partials_v2_kernel
-#endif
 
 __device__ __forceinline__ void flag_nonfinite(const DevicePlan &P, int tensor) {
   atomicOr(&P.status[tensor], LOPT_STATUS_NONFINITE_GRAD);
@@ -280,112 +277,6 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_partials_kernel(Devi
 }
 
 
-// ---------------------------------------------------------------------------
-// Factor partials, variant 2 (LOPT_FACTOR_V2): 16-byte loads straight into
-// registers, four rows in flight per thread, and a small shared footprint
-// (row partials of the item, the second half's column partials) so several
-// CTAs share an SM.  Thread t owns columns b0 + 4 (t % 128) .. +3 of every
-// row of parity t / 128: its column partials stay in registers, each row's
-// 512 columns are a warp shuffle tree per 128 columns plus a fixed-order sum
-// of the four warps.
-constexpr int kFactorV2MaxRows = 1024;
-struct FactorSmemV2 {
-  union {
-    double colbuf[kFactorWarps][kStripCols];   // the element-wise fallback
-    struct {
-      double rowred[kFactorV2MaxRows][4];
-      double colh[kStripCols];
-    } v;
-  };
-};
-
-// the element-wise fallback out of line: its 64 registers of row values and
-// f64 column sums do not raise the streaming path's register count
-__device__ __noinline__ void factor_tile_scalar_noinline(const DevicePlan &P, const FactorItem &it,
-                                                         const TensorDesc &T,
-                                                         double (*colbuf)[kStripCols]) {
-  factor_tile<false>(P, it, T, colbuf);
-}
-
-__device__ void factor_tile_v2(const DevicePlan &P, const FactorItem &it, const TensorDesc &T,
-                               FactorSmemV2 &F) {
-  const int tid = threadIdx.x, half = tid >> 7, c = tid & 127, lane = tid & 31;
-  const int wq = (tid >> 5) & 3;
-  __shared__ uint32_t bad_s;
-  if (tid == 0) bad_s = 0;
-  const int64_t n = T.n, width = it.b1 - it.b0, R = it.a1 - it.a0;
-  const int64_t col = it.b0 + 4 * c;
-  const bool colok = 4 * c < width;
-  double ca[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t r = half; r < R; r += 8) {
-    float4 x[4];
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int64_t rr = r + 2 * u;
-      x[u] = (rr < R && colok)
-                 ? __ldg(reinterpret_cast<const float4 *>(T.grad + (it.a0 + rr) * n + col))
-                 : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; u++) {
-      const int64_t rr = r + 2 * u;
-      if (rr >= R) break;   // uniform across the half
-      const int64_t row = it.a0 + rr;
-      double sq[4] = {(double)x[u].x * (double)x[u].x, (double)x[u].y * (double)x[u].y,
-                      (double)x[u].z * (double)x[u].z, (double)x[u].w * (double)x[u].w};
-      if (!(row * n >= T.lo && (row + 1) * n <= T.hi)) {
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-          const int64_t e = row * n + col + i;
-          if (e < T.lo || e >= T.hi) sq[i] = 0.0;
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 4; i++) ca[i] += sq[i];
-      const double rp = warp_sum((sq[0] + sq[1]) + (sq[2] + sq[3]));
-      if (lane == 0) F.v.rowred[rr][wq] = rp;
-    }
-  }
-  if (half == 1) {
-#pragma unroll
-    for (int i = 0; i < 4; i++) F.v.colh[4 * c + i] = ca[i];
-  }
-  __syncthreads();
-  if (half == 0 && colok) {
-#pragma unroll
-    for (int i = 0; i < 4; i++)
-      if (4 * c + i < width)
-        T.colpart[(int64_t)it.rowblock * n + col + i] = ca[i] + F.v.colh[4 * c + i];
-  }
-  bool bad = false;
-  for (int64_t r = tid; r < R; r += kFactorThreads) {
-    const double v = ((F.v.rowred[r][0] + F.v.rowred[r][1]) + F.v.rowred[r][2]) + F.v.rowred[r][3];
-    T.rowpart[(int64_t)it.strip * T.m + it.a0 + r] = v;
-    bad |= !isfinite(v);
-  }
-  if (bad) atomicOr(&bad_s, 1u);
-  __syncthreads();
-  if (tid == 0 && bad_s) flag_nonfinite(P, it.tensor);
-}
-
-__global__ void __launch_bounds__(kFactorThreads, 4) factor_partials_v2_kernel(DevicePlan P) {
-  extern __shared__ __align__(16) unsigned char factor_smem_raw[];
-  FactorSmemV2 &F = *reinterpret_cast<FactorSmemV2 *>(factor_smem_raw);
-  for (int item = blockIdx.x; item < P.n_factor_items; item += gridDim.x) {
-    const FactorItem it = P.factor_items[item];
-    const TensorDesc T = P.tensors[it.tensor];
-    if (T.n == 1) {
-      factor_vector(P, it, T);
-    } else if ((T.n & 3) == 0 && (reinterpret_cast<uintptr_t>(T.grad) & 15) == 0 &&
-               it.a1 - it.a0 <= kFactorV2MaxRows) {
-      factor_tile_v2(P, it, T, F);
-    } else {
-      factor_tile_scalar_noinline(P, it, T, F.colbuf);
-    }
-    __syncthreads();   // shared scratch is reused by the next item
-  }
-}
-
 // Tensor owning flattened work index idx: the last j with prefix[j] <= idx.
 __device__ __forceinline__ int tensor_of(const int64_t *prefix, int count, int64_t idx) {
   int lo = 0, hi = count;   // prefix[lo] <= idx < prefix[hi]
@@ -559,17 +450,6 @@ void launch_factor_partials(const DevicePlan &P, cudaStream_t s) {
   // one CTA per item (measured faster than a persistent grid: items differ in
   // size, and short CTAs backfill)
   (void)g_factor_sms;
-#if LOPT_FACTOR_V2
-  static bool attr2 = false;
-  if (!attr2) {
-    cudaFuncSetAttribute(factor_partials_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(FactorSmemV2));
-    attr2 = true;
-  }
-  if (P.n_factor_items > 0)
-    factor_partials_v2_kernel<<<P.n_factor_items, kFactorThreads, sizeof(FactorSmemV2), s>>>(P);
-  return;
-#endif
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(factor_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
