@@ -353,6 +353,11 @@ __device__ __forceinline__ float max_nan_abs(float m, float x) {
 constexpr int kTraceTiles = 64;
 constexpr int kTraceEvents = 12;
 __device__ long long g_trace[kTraceTiles][kTraceEvents];
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void trace(const DevicePlan &P, int32_t i, int ev) {
 #ifdef LOPT_TRACE
   if ((P.dbg & 32) && blockIdx.x == 0 && i < kTraceTiles && (threadIdx.x & 31) == 0)
@@ -822,6 +827,7 @@ struct __align__(1024) PairSmem {
   uint64_t img_full[kImgs];    // producer -> WGs: operand image loaded
   int32_t done[kPWGs][4];      // WG warps: last pair finished (image-buffer reuse)
   uint32_t tmem_base;
+  uint64_t t_start;            // CTA start (globaltimer), for the balance record
   // fused all-gather: each WG stages its pair's updated theta (double
   // buffered) for the 16-byte peer stores
   __align__(16) float peer_stage[kPWGs][2][2][128];
@@ -864,8 +870,13 @@ struct PairProducer {
     }
   }
   __device__ __forceinline__ void seek(const DevicePlan &P, int32_t t) {
-    int jj = 0;
-    while (jj + 1 < P.count && P.tensors[jj + 1].pair0 <= t) jj++;
+    // last tensor whose first pair is <= t (pair0 is non-decreasing)
+    int jj = 0, hi_ = P.count - 1;
+    while (jj < hi_) {
+      const int mid = (jj + hi_ + 1) >> 1;
+      if (P.tensors[mid].pair0 <= t) jj = mid;
+      else hi_ = mid - 1;
+    }
     while (P.tensors[jj].pairs == 0 && jj + 1 < P.count) jj++;
     load_tensor(P, jj, t - (int32_t)P.tensors[jj].pair0);
   }
@@ -1053,6 +1064,14 @@ __device__ __forceinline__ void pair_producer_loop(const DevicePlan &P, PairSmem
                    (uint32_t)sizeof(PrepImage), &S.img_full[img]);
         }
       }
+#ifdef LOPT_CTA_CLOCK
+      if (p == 0) {
+        long long *cp = &g_trace[0][0] + 5 * blockIdx.x;
+        if (i == 0) cp[2] = cp[3] = cp[4] = 0;
+        if (!pr.rb) cp[3]++;
+        if (!pr.aligned) cp[4]++;
+      }
+#endif
       if (i % kPProducers == p) {
         // parked in hardware while the ring is full (no issue slots spent)
         if (rc.wrapped) tc::mbar_sleep(&S.data_free[rc.i], rc.phase ^ 1u);
@@ -1061,11 +1080,19 @@ __device__ __forceinline__ void pair_producer_loop(const DevicePlan &P, PairSmem
       pr.advance(P);
       rc.next();
     }
+#ifdef LOPT_CTA_CLOCK
+    if (p == 0) (&g_trace[0][0] + 5 * blockIdx.x)[2] = k + 1;
+#endif
   }
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) {
+#ifdef LOPT_APPLY_MAXNREG
+#define LOPT_PAIR_BOUNDS __maxnreg__(LOPT_APPLY_MAXNREG)   // leaves registers for a co-resident kernel
+#else
+#define LOPT_PAIR_BOUNDS __launch_bounds__(kPThreads, 1)
+#endif
+__global__ void LOPT_PAIR_BOUNDS apply_pair_kernel(DevicePlan P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   PairSmem &S = *reinterpret_cast<PairSmem *>(smem_raw);
   const int tid = threadIdx.x;
@@ -1101,9 +1128,21 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+#ifdef LOPT_CTA_CLOCK
+  // per-CTA profile (balance experiments): start / end globaltimer, tensor
+  // switches, flat pairs, slow tiles of the CTA's range
+  long long *cta_prof = &g_trace[0][0] + 5 * blockIdx.x;
+  if (tid == 0) cta_prof[0] = (long long)globaltimer_ns();
+#endif
   const bool aborted = *P.abort_flag != 0;
-  const int32_t pb = (int32_t)(P.n_pairs * blockIdx.x / gridDim.x);
+  // this CTA's pairs: balanced by prep from the SMs' measured speeds
+#ifdef LOPT_EVEN_SPLIT
+  const int32_t pb = (int32_t)(P.n_pairs * blockIdx.x / gridDim.x);   // A/B reference
   const int32_t pe = (int32_t)(P.n_pairs * (blockIdx.x + 1) / gridDim.x);
+#else
+  const int32_t pb = P.pair_range[blockIdx.x], pe = P.pair_range[blockIdx.x + 1];
+#endif
+  if (tid == 0) S.t_start = globaltimer_ns();
   const int32_t np = aborted ? 0 : pe - pb;
 
   if (warp >= kPWarpProducer) {
@@ -1493,6 +1532,14 @@ __global__ void __launch_bounds__(kPThreads, 1) apply_pair_kernel(DevicePlan P) 
   }
   tc::fence_before_sync();
   __syncthreads();
+#ifdef LOPT_CTA_CLOCK
+  if (tid == 0) cta_prof[1] = (long long)globaltimer_ns();
+#endif
+  if (tid == 0) {
+    // this launch's speed record for the next split (none for an aborted step)
+    P.cta_perf[2 * blockIdx.x] = aborted ? 0 : pe - pb;
+    P.cta_perf[2 * blockIdx.x + 1] = (int64_t)(globaltimer_ns() - S.t_start);
+  }
   if (warp == 0) tc::tmem_dealloc(tbase, kTmemCols);
 }
 
@@ -1514,7 +1561,7 @@ void launch_tc_apply(const DevicePlan &P0, cudaStream_t s) {
   const int variant = ve ? atoi(ve) : 3;
   if (variant == 3) {
     const size_t smem = sizeof(PairSmem) + 1024;
-    const int pgrid = (int)std::min<int64_t>(g_num_sms, P.n_pairs);
+    const int pgrid = P.apply_grid;   // the grid prep balanced the ranges for
     if (P.kind == LOPT_SMALL_FC_LOPT) {
       cudaFuncSetAttribute(apply_pair_kernel<LOPT_SMALL_FC_LOPT>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

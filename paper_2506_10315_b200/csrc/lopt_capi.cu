@@ -104,7 +104,7 @@ struct lopt_plan {
   // workspace regions
   Region r_desc, r_fitems, r_sitems, r_aitems, r_tscal, r_step, r_status, r_maxabs, r_imaxabs,
       r_abort, r_fsums, r_rowpart, r_colpart, r_rowtab, r_coltab, r_statpart, r_sumsq, r_weights,
-      r_prep, r_bcsum, r_prefix;
+      r_prep, r_bcsum, r_prefix, r_range, r_perf;
   std::vector<int64_t> prefixes;   // red_prefix (count + 1) then fin_prefix (count + 1)
   size_t ws_bytes = 0;
   char *ws = nullptr;
@@ -355,6 +355,8 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   take(p->r_maxabs, sizeof(float) * count);
   take(p->r_imaxabs, sizeof(float) * std::max<size_t>(1, p->aitems.size()));
   take(p->r_abort, sizeof(uint32_t) * 4);
+  take(p->r_range, sizeof(int32_t) * (kMaxApplyCtas + 1));
+  take(p->r_perf, sizeof(int64_t) * 3 * kMaxApplyCtas);   // {pairs, ns} + smoothed speed
   take(p->r_fsums, sizeof(double) * (size_t)p->factor_sums);
   take(p->r_rowpart, sizeof(double) * (size_t)std::max<int64_t>(1, rowpart));
   take(p->r_colpart, sizeof(double) * (size_t)std::max<int64_t>(1, colpart));
@@ -394,6 +396,14 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   P.red_total = p->prefixes[count];
   P.fin_total = p->prefixes[2 * (size_t)count + 1];
   P.n_pairs = p->n_pairs;
+  {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+    cudaGetLastError();
+    P.apply_grid = (int32_t)std::min<int64_t>(std::min(sms, kMaxApplyCtas), p->n_pairs);
+  }
   if (fast && !fast_supported(P)) {
     delete p;
     return LOPT_ERR_UNSUPPORTED;
@@ -458,6 +468,8 @@ int lopt_bind_workspace(lopt_plan *p, void *dev_ptr, size_t bytes, void *stream)
   P.maxabs = (float *)(ws + p->r_maxabs.off);
   P.item_maxabs = (float *)(ws + p->r_imaxabs.off);
   P.abort_flag = (uint32_t *)(ws + p->r_abort.off);
+  P.pair_range = (int32_t *)(ws + p->r_range.off);
+  P.cta_perf = (int64_t *)(ws + p->r_perf.off);
   P.grad_flag = fsums + (p->factor_sums - 1);
   const bool fast = p->cfg.mode == LOPT_MODE_FAST;
   P.prep = fast ? (unsigned char *)(ws + p->r_prep.off) : nullptr;
@@ -470,6 +482,8 @@ int lopt_bind_workspace(lopt_plan *p, void *dev_ptr, size_t bytes, void *stream)
                                        cudaMemcpyHostToDevice, s))))
     return st;
   if ((st = check_cuda(cudaMemsetAsync(ws + p->r_bcsum.off, 0, p->r_bcsum.bytes, s)))) return st;
+  // no launch measured yet: prep splits the pairs evenly
+  if ((st = check_cuda(cudaMemsetAsync(ws + p->r_perf.off, 0, p->r_perf.bytes, s)))) return st;
   // descriptor uploads: pageable source, so the copies complete before return
   if ((st = check_cuda(cudaMemcpyAsync(P.tensors, p->descs.data(),
                                        sizeof(TensorDesc) * p->descs.size(),

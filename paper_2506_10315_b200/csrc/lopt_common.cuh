@@ -22,6 +22,7 @@ constexpr float kClip = 0.1f;         // features.py:82
 // hi/lo pairs {hi01, hi23, hi45, 0 | lo01, lo23, lo45, 0}
 constexpr int kRowTab = 16;
 constexpr int kWarpColumnBlocks = 32;   // factor reduce: warp-per-column threshold
+constexpr int kMaxApplyCtas = 256;   // pair-kernel CTAs with a balance record
 
 __host__ __device__ constexpr int d_feat(int kind) { return kind == LOPT_SMALL_FC_LOPT ? 39 : 29; }
 
@@ -118,6 +119,13 @@ struct DevicePlan {
   // fast path
   int64_t n_tiles;        // 128-element tiles over all tensors
   int64_t n_pairs;        // tile pairs over all tensors (pair kernel)
+  // pair-kernel balance: CTA b steps pairs [pair_range[b], pair_range[b + 1]);
+  // cta_perf[b] = {pairs, busy ns} of its last launch, from which prep
+  // computes the next ranges (SMs differ in speed)
+  int32_t *pair_range;    // [kMaxApplyCtas + 1]
+  int64_t *cta_perf;      // [kMaxApplyCtas x 2], then [kMaxApplyCtas] f64 smoothed speeds
+  int32_t apply_grid;     // pair-kernel CTAs (min(SMs, n_pairs))
+  int32_t pad_grid;
   unsigned char *prep;    // per-tensor PrepImage (B operands, layer-3 weights)
   double *bcsum;          // [count x d_feat] closed-form sums of broadcast features
   int32_t dbg, n_peers;   // dbg: timing experiments only (LOPT_APPLY_DEBUG), 0 in production

@@ -13,6 +13,9 @@
 //    from B operands prepared here once per tensor and step: the
 //    normalization scale folded into W1 (engine.py:686), a two-term bf16
 //    split of every weight, the canonical no-swizzle K-major UMMA layout.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
 #include "lopt_fast.cuh"
 
 namespace lopt {
@@ -23,7 +26,10 @@ namespace lopt {
 #ifndef LOPT_STAT_MINB
 #define LOPT_STAT_MINB 4       // stats CTAs per SM the registers are sized for
 #endif
-constexpr int kFastStatThreads = 256;
+#ifndef LOPT_STAT_THREADS
+#define LOPT_STAT_THREADS 256   // stats CTA size (co-residency experiments override)
+#endif
+constexpr int kFastStatThreads = LOPT_STAT_THREADS;
 constexpr int64_t kFastStatChunk = LOPT_STAT_CHUNK;
 
 __device__ __forceinline__ void split1(float x, uint16_t &hi, uint16_t &lo) {
@@ -52,9 +58,54 @@ __device__ __forceinline__ void prep_tab(float *tab, const float *sc) {
 // exponent s2, and the scaled broadcast-feature operands of every row/column.
 constexpr int kPrepThreads = 256;
 constexpr int kPrepSplit = 16;   // CTAs per tensor: the row/column table loops are latency-bound
+// The apply kernel's per-CTA pair ranges, from each CTA's measured speed
+// (pairs / busy ns) in the plan's previous launches (halved-weight average).  The SMs do not run at one
+// speed: over identical work ~12 % of them (the same CTA indices on every
+// box measured) take ~6 % longer (tools/cta_balance.py), and an even split
+// leaves the rest idle for their tail.  Speeds are clamped to [0.75, 1.33] x
+// their mean; missing records (first launch, aborted step) take the mean, so
+// the first launch splits evenly.  Any split gives identical results.
+static_assert(kPrepThreads >= kMaxApplyCtas, "one thread per apply CTA");
+__device__ void balance_pair_ranges(const DevicePlan &P) {
+  using Scan = cub::BlockScan<double, kPrepThreads>;
+  using Reduce = cub::BlockReduce<double, kPrepThreads>;
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Reduce::TempStorage red;
+  } tmp;
+  __shared__ double mean_s;
+  const int G = P.apply_grid, b = threadIdx.x;
+  // smoothed speed: the mean of the last record and the previous estimate
+  double *smooth = reinterpret_cast<double *>(P.cta_perf + 2 * kMaxApplyCtas);
+  double v = 0.0;
+  if (b < G) {
+    const int64_t n = P.cta_perf[2 * b], ns = P.cta_perf[2 * b + 1];
+    const double prev = smooth[b];
+    if (n > 0 && ns > 0) {
+      v = (double)n / (double)ns;
+      if (prev > 0.0) v = 0.5 * (v + prev);
+    } else {
+      v = prev;
+    }
+    smooth[b] = v;
+  }
+  const double sum = Reduce(tmp.red).Sum(v);
+  __syncthreads();
+  const double cnt = Reduce(tmp.red).Sum(v > 0.0 ? 1.0 : 0.0);
+  if (b == 0) mean_s = cnt > 0.0 ? sum / cnt : 1.0;
+  __syncthreads();
+  const double mean = mean_s;
+  if (b < G) v = v > 0.0 ? fmin(fmax(v, 0.75 * mean), 1.33 * mean) : mean;
+  double pre, total;
+  Scan(tmp.scan).ExclusiveSum(v, pre, total);
+  if (b < G) P.pair_range[b] = b == 0 ? 0 : (int32_t)((double)P.n_pairs * (pre / total));
+  if (b == 0) P.pair_range[G] = (int32_t)P.n_pairs;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(DevicePlan P) {
   constexpr int D = d_feat(KIND);
+  if (blockIdx.x == 0 && blockIdx.y == gridDim.y - 1 && P.apply_grid > 0) balance_pair_ranges(P);
   const int j = blockIdx.x;
   const TensorDesc T = P.tensors[j];
   PrepImage *img = reinterpret_cast<PrepImage *>(P.prep) + j;
