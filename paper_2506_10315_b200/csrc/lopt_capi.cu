@@ -229,6 +229,7 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   const bool fast = cfg->mode == LOPT_MODE_FAST;
   const int64_t stat_chunk = fast ? pick_stat_chunk(tensors, count) : strict_chunk(0);
   const int64_t apply_chunk = fast ? fast_apply_chunk() : strict_chunk(1);
+  const int64_t ftile = factor_tile_elems();
   int64_t rowpart = 0, colpart = 0, rows = 0, cols = 0;
   for (int j = 0; j < count; j++) {
     const lopt_tensor &t = tensors[j];
@@ -243,17 +244,17 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
     if (!cfg->state_advanced) {
       if (t.n == 1) {
         d.nstrips = 1;
-        d.nrowblocks = (int32_t)((t.m + factor_tile_elems() - 1) / factor_tile_elems());
+        d.nrowblocks = (int32_t)((t.m + ftile - 1) / ftile);
         for (int rb = 0; rb < d.nrowblocks; rb++) {
           // row blocks outside this call's element range keep zero partials
-          const int64_t r0 = rb * factor_tile_elems(), r1 = std::min<int64_t>(t.m, r0 + factor_tile_elems());
+          const int64_t r0 = rb * ftile, r1 = std::min<int64_t>(t.m, r0 + ftile);
           if (r1 <= t.lo || r0 >= t.hi) continue;
           FactorItem it{};
           it.tensor = j;
           it.strip = 0;
           it.rowblock = rb;
-          it.a0 = rb * factor_tile_elems();
-          it.a1 = std::min<int64_t>(t.m, it.a0 + factor_tile_elems());
+          it.a0 = rb * ftile;
+          it.a1 = std::min<int64_t>(t.m, it.a0 + ftile);
           it.b0 = 0;
           it.b1 = 1;
           p->fitems.push_back(it);
@@ -262,7 +263,7 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
         const int64_t strip = factor_strip_cols();
         d.nstrips = (int32_t)((t.n + strip - 1) / strip);
         const int64_t width = std::min<int64_t>(t.n, strip);
-        int64_t R = factor_tile_elems() / width;
+        int64_t R = ftile / width;
         R = std::max<int64_t>(8, (R + 7) / 8 * 8);
         d.nrowblocks = (int32_t)((t.m + R - 1) / R);
         for (int rb = 0; rb < d.nrowblocks; rb++)
@@ -338,6 +339,12 @@ int lopt_plan_create(const lopt_tensor *tensors, int32_t count, const lopt_confi
   p->factor_sums = rows + cols + 1;   // + the non-finite-gradient flag slot
   // workspace layout
   size_t off = 0;
+  // largest factor items first: the hardware dispatches CTAs in index order,
+  // so the small items (remainders, vectors) backfill the last wave.  Each
+  // item writes its own partial slots: the order does not change results.
+  std::stable_sort(p->fitems.begin(), p->fitems.end(), [](const FactorItem &x, const FactorItem &y) {
+    return (x.a1 - x.a0) * (x.b1 - x.b0) > (y.a1 - y.a0) * (y.b1 - y.b0);
+  });
   auto take = [&](Region &r, size_t bytes) {
     off = align_up(off, 256);
     r.off = off;
