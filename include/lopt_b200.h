@@ -143,6 +143,12 @@ int lopt_step(lopt_plan *plan, const lopt_step_args *args, void *stream);
  * dispatch (optim.py:144-180) for a launch-bound caller. */
 int lopt_graph_step(lopt_plan *plan, const lopt_step_args *args, void *stream);
 int lopt_graph_reset(lopt_plan *plan);
+/* Phase timing for a benchmark (no reference counterpart): with four CUDA
+ * events (cudaEvent_t, created by the caller) registered, every lopt_step
+ * records them before phase 1a, between phases 1a / 1b, 1b / 2 and after
+ * phase 2 on its stream -- the phases' GPU time without host gaps between
+ * them.  count 0 unregisters.  Not recorded inside a graph capture. */
+int lopt_set_phase_events(lopt_plan *plan, void *const *events, int32_t count);
 
 /* contiguous f64 blocks to all-reduce across element-sharded ranks */
 int lopt_factor_sums_ptr(lopt_plan *plan, double **ptr, int64_t *count);

@@ -121,6 +121,9 @@ struct lopt_plan {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaGraphNode_t gbegin = nullptr;
+  // benchmark phase events (lopt_set_phase_events)
+  cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int n_phase_ev = 0;
   void drop_graph() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
@@ -655,14 +658,36 @@ static int run_velo(lopt_plan *p, cudaStream_t s) {
   return st;
 }
 
+int lopt_set_phase_events(lopt_plan *p, void *const *events, int32_t count) {
+  if (!p || (count != 0 && count != 4) || (count && !events)) return LOPT_ERR_INVALID;
+  for (int k = 0; k < count; k++) {
+    if (!events[k]) return LOPT_ERR_INVALID;
+    p->phase_ev[k] = (cudaEvent_t)events[k];
+  }
+  p->n_phase_ev = count;
+  return LOPT_OK;
+}
+
 int lopt_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
   int st;
+  if (!p) return LOPT_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  bool tev = p->n_phase_ev == 4;
+  if (tev) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    tev = cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+  }
   if (args && (st = lopt_set_step_args(p, args, stream))) return st;
+  if (tev && (st = check_cuda(cudaEventRecord(p->phase_ev[0], s)))) return st;
   if ((st = lopt_factor_partials(p, stream))) return st;
   if ((st = lopt_factor_finalize(p, stream))) return st;
+  if (tev && (st = check_cuda(cudaEventRecord(p->phase_ev[1], s)))) return st;
   if ((st = lopt_feature_stats(p, stream))) return st;
-  if (p->velo && (st = run_velo(p, (cudaStream_t)stream))) return st;
-  return lopt_apply(p, stream);
+  if (tev && (st = check_cuda(cudaEventRecord(p->phase_ev[2], s)))) return st;
+  if (p->velo && (st = run_velo(p, s))) return st;
+  if ((st = lopt_apply(p, stream))) return st;
+  if (tev && (st = check_cuda(cudaEventRecord(p->phase_ev[3], s)))) return st;
+  return LOPT_OK;
 }
 
 int lopt_graph_step(lopt_plan *p, const lopt_step_args *args, void *stream) {

@@ -205,6 +205,20 @@ class StepPlan:
         _lib.check(self.L.lopt_step(self.h, ctypes.byref(self._args(lr, weight_decay, t)),
                                     _stream_handle()), "step")
 
+    def step_timed(self, lr: float, weight_decay: float, t: int, events):
+        """step() with four recorded torch.cuda.Events (enable_timing) around
+        phases 1a (factors), 1b (feature statistics) and 2 (apply) -- recorded
+        by the C step on its stream, so no host gaps fall inside a phase."""
+        for e in events:
+            if e.cuda_event == 0:
+                e.record()   # torch creates the CUDA event on first record
+        arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in events])
+        _lib.check(self.L.lopt_set_phase_events(self.h, arr, 4), "set_phase_events")
+        try:
+            self.step(lr, weight_decay, t)
+        finally:
+            _lib.check(self.L.lopt_set_phase_events(self.h, None, 0), "set_phase_events")
+
     def graph_step(self, lr: float, weight_decay: float, t: int):
         """step() replayed from the plan's captured CUDA graph (one launch)."""
         _lib.check(self.L.lopt_graph_step(self.h, ctypes.byref(self._args(lr, weight_decay, t)),

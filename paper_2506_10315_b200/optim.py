@@ -245,6 +245,13 @@ class LearnedOptimizer(torch.optim.Optimizer):
             else:
                 plan.step(lr, weight_decay, t)
             return
+        if self._after_stats is None:
+            # one C step recording the phase events on the stream
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            plan.step_timed(lr, weight_decay, t, ev)
+            for k, name in enumerate(("factors", "stats", "apply")):
+                self.phase_events.append((name, ev[k], ev[k + 1]))
+            return
         plan.set_step(lr, weight_decay, t)
         self._timed("factors", lambda: (plan.factor_partials(), plan.factor_finalize()))
         self._timed("stats", plan.feature_stats)
