@@ -218,39 +218,57 @@ def step_kwargs(opt):
 
 def time_device(opt, params, grads, steps, warmup, world):
     """Device-resident inputs; CUDA events on the current stream.  The timed
-    steps are plain optimizer.step() calls (one C call each); a second,
-    separately timed pass records per-phase events for the roofline."""
+    steps are plain optimizer.step() calls (one graph launch each on one
+    device).  On one device they also record their own phase events (event
+    nodes inside the captured graph); a sharded step (Python between its
+    phases and collectives) records phases in a second pass instead, so the
+    headline loop carries no per-phase host work."""
     import torch
 
     for p, g in zip(params, grads):
         p.grad = g
     kw = step_kwargs(opt)
+    # the timed steps record their own phase events (inside the captured graph
+    # on one device), so the phase times -- the roofline's apply duration --
+    # come from the measured steps themselves; warm-up captures that graph
+    inline_phases = world == 1
+    opt.phase_events = [] if inline_phases else None
     for _ in range(warmup):
         opt.step(**kw)
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
+    opt.phase_events = [] if inline_phases else None
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
-    h0 = time.perf_counter()
-    for _ in range(steps):
-        opt.step(**kw)
-    host_ms = (time.perf_counter() - h0) * 1e3 / steps   # enqueue cost (no sync inside)
-    end.record()
-    torch.cuda.synchronize()
-    barrier(world)
-    ms = start.elapsed_time(end)
-    opt.phase_events = []
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    start.record()
     marks[0].record()
     for k in range(steps):
         opt.step(**kw)
         marks[k + 1].record()
+    end.record()
     torch.cuda.synchronize()
+    barrier(world)
+    ms = start.elapsed_time(end)
+    if not inline_phases:
+        opt.phase_events = []
+        for _ in range(steps):
+            opt.step(**kw)
+        torch.cuda.synchronize()
     phases = {}
     for name, a, b in opt.phase_events:
         phases.setdefault(name, []).append(a.elapsed_time(b))
     opt.phase_events = None
+    # host enqueue cost per step (no sync inside), plain steps
+    for _ in range(2):
+        opt.step(**kw)
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    for _ in range(steps):
+        opt.step(**kw)
+    host_ms = (time.perf_counter() - h0) * 1e3 / steps
+    torch.cuda.synchronize()
+    barrier(world)
     per_step = sorted(marks[k].elapsed_time(marks[k + 1]) for k in range(steps))
     if world > 1 and hasattr(opt, "set_exchange"):
         # SURVEY.md §8(e): the same step without the parameter exchange

@@ -143,11 +143,14 @@ int lopt_step(lopt_plan *plan, const lopt_step_args *args, void *stream);
  * dispatch (optim.py:144-180) for a launch-bound caller. */
 int lopt_graph_step(lopt_plan *plan, const lopt_step_args *args, void *stream);
 int lopt_graph_reset(lopt_plan *plan);
-/* Phase timing for a benchmark (no reference counterpart): with four CUDA
- * events (cudaEvent_t, created by the caller) registered, every lopt_step
- * records them before phase 1a, between phases 1a / 1b, 1b / 2 and after
- * phase 2 on its stream -- the phases' GPU time without host gaps between
- * them.  count 0 unregisters.  Not recorded inside a graph capture. */
+/* Phase timing for a benchmark (no reference counterpart): with five CUDA
+ * events (cudaEvent_t, created by the caller with timing) registered, every
+ * lopt_step / lopt_graph_step records them on its stream before phase 1a,
+ * after 1a (factors), after 1b (feature statistics), after the VeLO
+ * hypernetwork and after phase 2 (apply) -- the phases' GPU time inside the
+ * measured steps.  A graph captured with events holds event-record nodes that
+ * each lopt_graph_step re-points to the registered events.  count 0
+ * unregisters; changing between 0 and 5 recaptures the graph. */
 int lopt_set_phase_events(lopt_plan *plan, void *const *events, int32_t count);
 
 /* contiguous f64 blocks to all-reduce across element-sharded ranks */

@@ -121,15 +121,19 @@ struct lopt_plan {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaGraphNode_t gbegin = nullptr;
-  // benchmark phase events (lopt_set_phase_events)
-  cudaEvent_t phase_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // benchmark phase events (lopt_set_phase_events) and, in a graph captured
+  // with them, the event-record nodes re-pointed before every launch
+  cudaEvent_t phase_ev[5] = {};
   int n_phase_ev = 0;
+  cudaGraphNode_t ev_node[5] = {};
+  bool graph_ev = false;
   void drop_graph() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
     gexec = nullptr;
     graph = nullptr;
     gbegin = nullptr;
+    graph_ev = false;
   }
   ~lopt_plan() {
     drop_graph();
@@ -659,11 +663,12 @@ static int run_velo(lopt_plan *p, cudaStream_t s) {
 }
 
 int lopt_set_phase_events(lopt_plan *p, void *const *events, int32_t count) {
-  if (!p || (count != 0 && count != 4) || (count && !events)) return LOPT_ERR_INVALID;
-  for (int k = 0; k < count; k++) {
+  if (!p || (count != 0 && count != 5) || (count && !events)) return LOPT_ERR_INVALID;
+  for (int k = 0; k < count; k++)
     if (!events[k]) return LOPT_ERR_INVALID;
-    p->phase_ev[k] = (cudaEvent_t)events[k];
-  }
+  // a captured step with(out) event nodes no longer matches: recapture
+  if (p->gexec && (count == 5) != p->graph_ev) p->drop_graph();
+  for (int k = 0; k < count; k++) p->phase_ev[k] = (cudaEvent_t)events[k];
   p->n_phase_ev = count;
   return LOPT_OK;
 }
@@ -672,22 +677,30 @@ int lopt_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
   int st;
   if (!p) return LOPT_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  bool tev = p->n_phase_ev == 4;
+  const bool tev = p->n_phase_ev == 5;
+  bool capturing = false;
   if (tev) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    tev = cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+    if ((st = check_cuda(cudaStreamIsCapturing(s, &cs)))) return st;
+    capturing = cs != cudaStreamCaptureStatusNone;
   }
+  // inside a capture the records become event-record nodes (external events)
+  auto mark = [&](int k) {
+    if (!tev) return LOPT_OK;
+    return check_cuda(capturing ? cudaEventRecordWithFlags(p->phase_ev[k], s, cudaEventRecordExternal)
+                                : cudaEventRecord(p->phase_ev[k], s));
+  };
   if (args && (st = lopt_set_step_args(p, args, stream))) return st;
-  if (tev && (st = check_cuda(cudaEventRecord(p->phase_ev[0], s)))) return st;
+  if ((st = mark(0))) return st;
   if ((st = lopt_factor_partials(p, stream))) return st;
   if ((st = lopt_factor_finalize(p, stream))) return st;
-  if (tev && (st = check_cuda(cudaEventRecord(p->phase_ev[1], s)))) return st;
+  if ((st = mark(1))) return st;
   if ((st = lopt_feature_stats(p, stream))) return st;
-  if (tev && (st = check_cuda(cudaEventRecord(p->phase_ev[2], s)))) return st;
+  if ((st = mark(2))) return st;
   if (p->velo && (st = run_velo(p, s))) return st;
+  if ((st = mark(3))) return st;
   if ((st = lopt_apply(p, stream))) return st;
-  if (tev && (st = check_cuda(cudaEventRecord(p->phase_ev[3], s)))) return st;
-  return LOPT_OK;
+  return mark(4);
 }
 
 int lopt_graph_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
@@ -729,7 +742,35 @@ int lopt_graph_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
       return st ? st : LOPT_ERR_CUDA;
     }
     p->gbegin = root;
+    if (p->n_phase_ev == 5) {
+      // map the captured event-record nodes to the phase marks
+      size_t nn = 0;
+      if ((st = check_cuda(cudaGraphGetNodes(g, nullptr, &nn)))) return st;
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if ((st = check_cuda(cudaGraphGetNodes(g, nodes.data(), &nn)))) return st;
+      int found = 0;
+      for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t ev = nullptr;
+        if (cudaGraphEventRecordNodeGetEvent(nd, &ev) != cudaSuccess) continue;
+        for (int k = 0; k < 5; k++)
+          if (ev == p->phase_ev[k]) {
+            p->ev_node[k] = nd;
+            found |= 1 << k;
+          }
+      }
+      if (found != 31) {
+        p->drop_graph();
+        return LOPT_ERR_CUDA;
+      }
+      p->graph_ev = true;
+    }
   }
+  if (p->graph_ev)
+    for (int k = 0; k < 5; k++)
+      if ((st = check_cuda(cudaGraphExecEventRecordNodeSetEvent(p->gexec, p->ev_node[k], p->phase_ev[k]))))
+        return st;
   cudaKernelNodeParams kp{};
   if ((st = check_cuda(cudaGraphKernelNodeGetParams(p->gbegin, &kp)))) return st;
   int32_t one = 1;

@@ -205,19 +205,26 @@ class StepPlan:
         _lib.check(self.L.lopt_step(self.h, ctypes.byref(self._args(lr, weight_decay, t)),
                                     _stream_handle()), "step")
 
-    def step_timed(self, lr: float, weight_decay: float, t: int, events):
-        """step() with four recorded torch.cuda.Events (enable_timing) around
-        phases 1a (factors), 1b (feature statistics) and 2 (apply) -- recorded
-        by the C step on its stream, so no host gaps fall inside a phase."""
+    def step_timed(self, lr: float, weight_decay: float, t: int, events, graph: bool = True):
+        """step() (graph=False) or graph_step() recording five torch.cuda.Events
+        (enable_timing) around the phases: factors, feature statistics, VeLO
+        hypernetwork, apply (lopt_set_phase_events).  The events stay
+        registered (and referenced) until clear_phase_events()."""
         for e in events:
             if e.cuda_event == 0:
                 e.record()   # torch creates the CUDA event on first record
-        arr = (ctypes.c_void_p * 4)(*[e.cuda_event for e in events])
-        _lib.check(self.L.lopt_set_phase_events(self.h, arr, 4), "set_phase_events")
-        try:
+        arr = (ctypes.c_void_p * 5)(*[e.cuda_event for e in events])
+        _lib.check(self.L.lopt_set_phase_events(self.h, arr, 5), "set_phase_events")
+        self._phase_refs = list(events)
+        if graph:
+            self.graph_step(lr, weight_decay, t)
+        else:
             self.step(lr, weight_decay, t)
-        finally:
+
+    def clear_phase_events(self):
+        if getattr(self, "_phase_refs", None) is not None:
             _lib.check(self.L.lopt_set_phase_events(self.h, None, 0), "set_phase_events")
+            self._phase_refs = None
 
     def graph_step(self, lr: float, weight_decay: float, t: int):
         """step() replayed from the plan's captured CUDA graph (one launch)."""

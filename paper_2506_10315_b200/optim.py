@@ -238,19 +238,24 @@ class LearnedOptimizer(torch.optim.Optimizer):
         return self._after_stats is None
 
     def _run_plan(self, plan, lr, weight_decay, t, gi, params):
-        if self.phase_events is None and self._single_call(gi, plan, params):
+        if self._single_call(gi, plan, params):
+            if self.phase_events is not None:
+                # phase events recorded by the C step itself (inside the
+                # captured graph when use_graph), so the phase times come from
+                # the very steps being measured
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                plan.step_timed(lr, weight_decay, t, ev, graph=self.use_graph)
+                names = ("factors", "stats", "hypernet", "apply")
+                for k, name in enumerate(names):
+                    if name != "hypernet" or self._after_stats is not None:
+                        self.phase_events.append((name, ev[k], ev[k + 1]))
+                return
+            plan.clear_phase_events()
             # one C call: all phases (from the captured graph after the first)
             if self.use_graph:
                 plan.graph_step(lr, weight_decay, t)
             else:
                 plan.step(lr, weight_decay, t)
-            return
-        if self._after_stats is None:
-            # one C step recording the phase events on the stream
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            plan.step_timed(lr, weight_decay, t, ev)
-            for k, name in enumerate(("factors", "stats", "apply")):
-                self.phase_events.append((name, ev[k], ev[k + 1]))
             return
         plan.set_step(lr, weight_decay, t)
         self._timed("factors", lambda: (plan.factor_partials(), plan.factor_finalize()))

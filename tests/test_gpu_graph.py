@@ -89,27 +89,33 @@ def test_graph_step_nonfinite_gradient_changes_nothing():
     assert torch.isfinite(a).all() and not torch.equal(a.detach(), snap)
 
 
-def test_phase_timed_step_equals_graph_step():
-    """The benchmark's phase-timed step (lopt_set_phase_events: one C step
-    recording four events) updates exactly like the graph step, and its phase
-    windows are positive and add up to the step."""
+@pytest.mark.parametrize("velo", [False, True])
+def test_phase_timed_graph_step_equals_plain_step(velo):
+    """The benchmark's phase-timed step (lopt_set_phase_events: event-record
+    nodes inside the captured graph, re-pointed every launch) updates exactly
+    like the plain kernel-by-kernel step, and its phase windows are positive."""
     import torch
 
     import paper_2506_10315_b200 as P
 
-    rng, runs = _pair(P, "fast", "small_fc_lopt")
-    for k in range(4):
+    rng, runs = _pair(P, "fast", "velo_mlp" if velo else "small_fc_lopt", velo)
+    names_want = ["factors", "stats", "hypernet", "apply"] if velo else ["factors", "stats", "apply"]
+    for k in range(5):
         gs = [np.asarray(rng.standard_normal(s) * 1e-2, F32) for s in SHAPES]
         for j, (ps, opt) in enumerate(runs):
             for p, g in zip(ps, gs):
                 p.grad = torch.from_numpy(g).cuda()
-            opt.phase_events = [] if j == 1 else None
-            opt.step()
-            if j == 1:
+            timed = j == 0 and k != 3   # graph run; one plain step in between
+            opt.phase_events = [] if timed else None
+            if velo:
+                opt.step(loss=1.5 - 0.1 * k)
+            else:
+                opt.step()
+            if timed:
                 torch.cuda.synchronize()
-                names = [n for n, _, _ in opt.phase_events]
-                assert names == ["factors", "stats", "apply"]
-                assert all(a.elapsed_time(b) > 0.0 for _, a, b in opt.phase_events)
+                assert [n for n, _, _ in opt.phase_events] == names_want
+                assert all(a.elapsed_time(b) >= 0.0 for _, a, b in opt.phase_events)
+                assert sum(a.elapsed_time(b) for _, a, b in opt.phase_events) > 0.0
                 opt.phase_events = None
     for a, b in zip(runs[0][0], runs[1][0]):
         assert torch.equal(a.detach(), b.detach())
