@@ -143,15 +143,19 @@ int lopt_step(lopt_plan *plan, const lopt_step_args *args, void *stream);
  * dispatch (optim.py:144-180) for a launch-bound caller. */
 int lopt_graph_step(lopt_plan *plan, const lopt_step_args *args, void *stream);
 int lopt_graph_reset(lopt_plan *plan);
-/* Phase timing for a benchmark (no reference counterpart): with five CUDA
- * events (cudaEvent_t, created by the caller with timing) registered, every
- * lopt_step / lopt_graph_step records them on its stream before phase 1a,
+/* Phase timing for a benchmark (no reference counterpart).  With `slots` > 0
+ * the plan owns slots x 5 timing events; each lopt_step / lopt_graph_step
+ * uses the next set in turn and records it on its stream before phase 1a,
  * after 1a (factors), after 1b (feature statistics), after the VeLO
- * hypernetwork and after phase 2 (apply) -- the phases' GPU time inside the
- * measured steps.  A graph captured with events holds event-record nodes that
- * each lopt_graph_step re-points to the registered events.  count 0
- * unregisters; changing between 0 and 5 recaptures the graph. */
-int lopt_set_phase_events(lopt_plan *plan, void *const *events, int32_t count);
+ * hypernetwork and after phase 2 (apply) -- phase times of the measured steps
+ * themselves (a graph captured with timing holds event-record nodes,
+ * re-pointed to the step's set before every launch).  slots 0 turns it off;
+ * turning it on or off recaptures the graph.  lopt_phase_slot: the set the
+ * next step uses; lopt_phase_elapsed: ms between marks k0 and k1 (0-4) of a
+ * set, once that step completed. */
+int lopt_set_phase_timing(lopt_plan *plan, int32_t slots);
+int lopt_phase_slot(const lopt_plan *plan, int32_t *next_slot);
+int lopt_phase_elapsed(lopt_plan *plan, int32_t slot, int32_t k0, int32_t k1, float *ms);
 
 /* contiguous f64 blocks to all-reduce across element-sharded ranks */
 int lopt_factor_sums_ptr(lopt_plan *plan, double **ptr, int64_t *count);

@@ -37,7 +37,8 @@ EXPORTS = [
     "lopt_probe_umma", "lopt_selftest_expf", "lopt_set_peers", "lopt_graph_step",
     "lopt_graph_reset", "lopt_set_velo", "lopt_probe_tmem", "lopt_adam_step",
     "lopt_adafactor_step", "lopt_adafactor_scratch_bytes", "lopt_set_stat_counts",
-    "lopt_enable_peer_access", "lopt_set_phase_events",
+    "lopt_enable_peer_access", "lopt_set_phase_timing", "lopt_phase_slot",
+    "lopt_phase_elapsed",
 ]
 
 
@@ -139,7 +140,9 @@ def lib(required: bool = True):
     L.lopt_selftest_expf.argtypes = [vp, vp, ctypes.c_int64, vp]
     L.lopt_graph_step.argtypes = [vp, ctypes.POINTER(lopt_step_args), vp]
     L.lopt_graph_reset.argtypes = [vp]
-    L.lopt_set_phase_events.argtypes = [vp, vp, i32]
+    L.lopt_set_phase_timing.argtypes = [vp, i32]
+    L.lopt_phase_slot.argtypes = [vp, ctypes.POINTER(i32)]
+    L.lopt_phase_elapsed.argtypes = [vp, i32, i32, i32, ctypes.POINTER(ctypes.c_float)]
     L.lopt_set_velo.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp]
     for name in EXPORTS:
         f = getattr(L, name)

@@ -121,12 +121,19 @@ struct lopt_plan {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
   cudaGraphNode_t gbegin = nullptr;
-  // benchmark phase events (lopt_set_phase_events) and, in a graph captured
-  // with them, the event-record nodes re-pointed before every launch
-  cudaEvent_t phase_ev[5] = {};
-  int n_phase_ev = 0;
+  // benchmark phase timing (lopt_set_phase_timing): `ev_slots` sets of five
+  // plan-owned events, one set per step in turn; a graph captured with timing
+  // holds event-record nodes re-pointed to the step's set before each launch
+  std::vector<cudaEvent_t> phase_ev;   // [ev_slots x 5]
+  int ev_slots = 0;
+  int64_t ev_step = 0;                 // steps recorded so far
   cudaGraphNode_t ev_node[5] = {};
   bool graph_ev = false;
+  void drop_events() {
+    for (cudaEvent_t e : phase_ev) cudaEventDestroy(e);
+    phase_ev.clear();
+    ev_slots = 0;
+  }
   void drop_graph() {
     if (gexec) cudaGraphExecDestroy(gexec);
     if (graph) cudaGraphDestroy(graph);
@@ -137,17 +144,19 @@ struct lopt_plan {
   }
   ~lopt_plan() {
     drop_graph();
+    drop_events();
     if (cap_stream) cudaStreamDestroy(cap_stream);
   }
 };
 
-static int check_cuda(cudaError_t e) {
+static int check_cuda_at(cudaError_t e, int line) {
   if (e != cudaSuccess) {
-    fprintf(stderr, "lopt_b200: CUDA error %s\n", cudaGetErrorString(e));
+    fprintf(stderr, "lopt_b200: CUDA error %s (lopt_capi.cu:%d)\n", cudaGetErrorString(e), line);
     return LOPT_ERR_CUDA;
   }
   return LOPT_OK;
 }
+#define check_cuda(e) check_cuda_at((e), __LINE__)
 
 static int check_launch() { return check_cuda(cudaGetLastError()); }
 
@@ -662,22 +671,43 @@ static int run_velo(lopt_plan *p, cudaStream_t s) {
   return st;
 }
 
-int lopt_set_phase_events(lopt_plan *p, void *const *events, int32_t count) {
-  if (!p || (count != 0 && count != 5) || (count && !events)) return LOPT_ERR_INVALID;
-  for (int k = 0; k < count; k++)
-    if (!events[k]) return LOPT_ERR_INVALID;
+int lopt_set_phase_timing(lopt_plan *p, int32_t slots) {
+  if (!p || slots < 0 || slots > 4096) return LOPT_ERR_INVALID;
   // a captured step with(out) event nodes no longer matches: recapture
-  if (p->gexec && (count == 5) != p->graph_ev) p->drop_graph();
-  for (int k = 0; k < count; k++) p->phase_ev[k] = (cudaEvent_t)events[k];
-  p->n_phase_ev = count;
+  if (p->gexec && (slots > 0) != p->graph_ev) p->drop_graph();
+  p->drop_events();
+  for (int i = 0; i < 5 * slots; i++) {
+    cudaEvent_t e = nullptr;
+    int st;
+    if ((st = check_cuda(cudaEventCreate(&e)))) {
+      p->drop_events();
+      return st;
+    }
+    p->phase_ev.push_back(e);
+  }
+  p->ev_slots = slots;
+  p->ev_step = 0;
   return LOPT_OK;
+}
+
+int lopt_phase_slot(const lopt_plan *p, int32_t *next_slot) {
+  if (!p || !next_slot || p->ev_slots == 0) return LOPT_ERR_INVALID;
+  *next_slot = (int32_t)(p->ev_step % p->ev_slots);
+  return LOPT_OK;
+}
+
+int lopt_phase_elapsed(lopt_plan *p, int32_t slot, int32_t k0, int32_t k1, float *ms) {
+  if (!p || !ms || slot < 0 || slot >= p->ev_slots || k0 < 0 || k1 < 0 || k0 > 4 || k1 > 4)
+    return LOPT_ERR_INVALID;
+  return check_cuda(cudaEventElapsedTime(ms, p->phase_ev[5 * slot + k0], p->phase_ev[5 * slot + k1]));
 }
 
 int lopt_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
   int st;
   if (!p) return LOPT_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
-  const bool tev = p->n_phase_ev == 5;
+  const bool tev = p->ev_slots > 0;
+  const int slot = tev ? (int)(p->ev_step % p->ev_slots) : 0;
   bool capturing = false;
   if (tev) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -687,8 +717,9 @@ int lopt_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
   // inside a capture the records become event-record nodes (external events)
   auto mark = [&](int k) {
     if (!tev) return LOPT_OK;
-    return check_cuda(capturing ? cudaEventRecordWithFlags(p->phase_ev[k], s, cudaEventRecordExternal)
-                                : cudaEventRecord(p->phase_ev[k], s));
+    cudaEvent_t e = p->phase_ev[5 * slot + k];
+    return check_cuda(capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+                                : cudaEventRecord(e, s));
   };
   if (args && (st = lopt_set_step_args(p, args, stream))) return st;
   if ((st = mark(0))) return st;
@@ -700,7 +731,9 @@ int lopt_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
   if (p->velo && (st = run_velo(p, s))) return st;
   if ((st = mark(3))) return st;
   if ((st = lopt_apply(p, stream))) return st;
-  return mark(4);
+  if ((st = mark(4))) return st;
+  if (tev && !capturing) p->ev_step++;
+  return LOPT_OK;
 }
 
 int lopt_graph_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
@@ -742,7 +775,7 @@ int lopt_graph_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
       return st ? st : LOPT_ERR_CUDA;
     }
     p->gbegin = root;
-    if (p->n_phase_ev == 5) {
+    if (p->ev_slots > 0) {
       // map the captured event-record nodes to the phase marks
       size_t nn = 0;
       if ((st = check_cuda(cudaGraphGetNodes(g, nullptr, &nn)))) return st;
@@ -754,8 +787,9 @@ int lopt_graph_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
         if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeEventRecord) continue;
         cudaEvent_t ev = nullptr;
         if (cudaGraphEventRecordNodeGetEvent(nd, &ev) != cudaSuccess) continue;
+        const int cs = (int)(p->ev_step % p->ev_slots);
         for (int k = 0; k < 5; k++)
-          if (ev == p->phase_ev[k]) {
+          if (ev == p->phase_ev[5 * cs + k]) {
             p->ev_node[k] = nd;
             found |= 1 << k;
           }
@@ -767,10 +801,14 @@ int lopt_graph_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
       p->graph_ev = true;
     }
   }
-  if (p->graph_ev)
+  if (p->graph_ev) {
+    const int slot = (int)(p->ev_step % p->ev_slots);
     for (int k = 0; k < 5; k++)
-      if ((st = check_cuda(cudaGraphExecEventRecordNodeSetEvent(p->gexec, p->ev_node[k], p->phase_ev[k]))))
+      if ((st = check_cuda(cudaGraphExecEventRecordNodeSetEvent(p->gexec, p->ev_node[k],
+                                                                  p->phase_ev[5 * slot + k]))))
         return st;
+    p->ev_step++;
+  }
   cudaKernelNodeParams kp{};
   if ((st = check_cuda(cudaGraphKernelNodeGetParams(p->gbegin, &kp)))) return st;
   int32_t one = 1;

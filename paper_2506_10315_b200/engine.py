@@ -80,6 +80,20 @@ class Slot:
             col_factors=self.c.data_ptr(), weight_slot=self.weight_slot, reserved=0)
 
 
+class PhaseMark:
+    """One of a timed step's phase events (StepPlan.step_timed); like
+    torch.cuda.Event.elapsed_time, in ms."""
+
+    def __init__(self, plan, slot: int, k: int):
+        self.plan, self.slot, self.k = plan, slot, k
+
+    def elapsed_time(self, other: "PhaseMark") -> float:
+        ms = ctypes.c_float()
+        _lib.check(self.plan.L.lopt_phase_elapsed(self.plan.h, self.slot, self.k, other.k,
+                                                  ctypes.byref(ms)), "phase_elapsed")
+        return float(ms.value)
+
+
 class StepPlan:
     """A compiled step over fixed tensors (OptimizerHandle of optim.py:104-141)."""
 
@@ -205,26 +219,31 @@ class StepPlan:
         _lib.check(self.L.lopt_step(self.h, ctypes.byref(self._args(lr, weight_decay, t)),
                                     _stream_handle()), "step")
 
-    def step_timed(self, lr: float, weight_decay: float, t: int, events, graph: bool = True):
-        """step() (graph=False) or graph_step() recording five torch.cuda.Events
-        (enable_timing) around the phases: factors, feature statistics, VeLO
-        hypernetwork, apply (lopt_set_phase_events).  The events stay
-        registered (and referenced) until clear_phase_events()."""
-        for e in events:
-            if e.cuda_event == 0:
-                e.record()   # torch creates the CUDA event on first record
-        arr = (ctypes.c_void_p * 5)(*[e.cuda_event for e in events])
-        _lib.check(self.L.lopt_set_phase_events(self.h, arr, 5), "set_phase_events")
-        self._phase_refs = list(events)
+    def step_timed(self, lr: float, weight_decay: float, t: int, graph: bool = True,
+                   slots: int = 512):
+        """step() (graph=False) or graph_step() recording the plan's phase
+        events (lopt_set_phase_timing): returns five PhaseMarks -- before the
+        factors, after the factors, after the feature statistics, after the
+        VeLO hypernetwork, after the apply pass -- whose elapsed_time() is
+        valid once the step completed.  A plan keeps `slots` event sets; read
+        the marks before that many further timed steps reuse them."""
+        if getattr(self, "_ev_slots", 0) == 0:
+            _lib.check(self.L.lopt_set_phase_timing(self.h, int(slots)), "set_phase_timing")
+            self._ev_slots = int(slots)
+        slot = ctypes.c_int32()
+        _lib.check(self.L.lopt_phase_slot(self.h, ctypes.byref(slot)), "phase_slot")
         if graph:
             self.graph_step(lr, weight_decay, t)
         else:
             self.step(lr, weight_decay, t)
+        return [PhaseMark(self, slot.value, k) for k in range(5)]
 
     def clear_phase_events(self):
-        if getattr(self, "_phase_refs", None) is not None:
-            _lib.check(self.L.lopt_set_phase_events(self.h, None, 0), "set_phase_events")
-            self._phase_refs = None
+        """Turn phase timing off (the next graph step recaptures without
+        event nodes)."""
+        if getattr(self, "_ev_slots", 0):
+            _lib.check(self.L.lopt_set_phase_timing(self.h, 0), "set_phase_timing")
+            self._ev_slots = 0
 
     def graph_step(self, lr: float, weight_decay: float, t: int):
         """step() replayed from the plan's captured CUDA graph (one launch)."""

@@ -243,8 +243,7 @@ class LearnedOptimizer(torch.optim.Optimizer):
                 # phase events recorded by the C step itself (inside the
                 # captured graph when use_graph), so the phase times come from
                 # the very steps being measured
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-                plan.step_timed(lr, weight_decay, t, ev, graph=self.use_graph)
+                ev = plan.step_timed(lr, weight_decay, t, graph=self.use_graph)
                 names = ("factors", "stats", "hypernet", "apply")
                 for k, name in enumerate(names):
                     if name != "hypernet" or self._after_stats is not None:
