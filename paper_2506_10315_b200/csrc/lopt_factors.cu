@@ -138,6 +138,8 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// WFULL: the item spans a full 512-column strip (no per-column bounds)
+template <bool WFULL>
 __device__ void factor_tile_async(const DevicePlan &P, const FactorItem &it, const TensorDesc &T,
                                   FactorSmem &F) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -160,7 +162,7 @@ __device__ void factor_tile_async(const DevicePlan &P, const FactorItem &it, con
 #pragma unroll
         for (int k = 0; k < 4; k++) {
           const int b = 4 * lane + 128 * k;
-          if (b < width) cp_async16(&F.rows[warp][buf][r][lane + 32 * k], g + b);
+          if (WFULL || b < width) cp_async16(&F.rows[warp][buf][r][lane + 32 * k], g + b);
         }
       }
     }
@@ -185,18 +187,23 @@ __device__ void factor_tile_async(const DevicePlan &P, const FactorItem &it, con
       for (int k = 0; k < 4; k++) {
         const int b = 4 * lane + 128 * k;
         float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (b < width) x = F.rows[warp][buf][r][lane + 32 * k];
+        if (WFULL || b < width) x = F.rows[warp][buf][r][lane + 32 * k];
         v[4 * k + 0] = x.x; v[4 * k + 1] = x.y; v[4 * k + 2] = x.z; v[4 * k + 3] = x.w;
       }
       const bool full = row * n >= T.lo && (row + 1) * n <= T.hi;
+      if (!full) {
+        // a row cut by the element range: elements outside it count zero
+        // (masked once here, so the accumulation below has no branches)
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+          const int64_t e = row * n + col_of<true>(it.b0, lane, k);
+          if (e < T.lo || e >= T.hi) v[k] = 0.0f;
+        }
+      }
       double rowp2[2] = {0.0, 0.0};
 #pragma unroll
       for (int k = 0; k < 16; k++) {
-        double sq = (double)v[k] * (double)v[k];
-        if (!full) {
-          const int64_t e = row * n + col_of<true>(it.b0, lane, k);
-          if (e < T.lo || e >= T.hi) sq = 0.0;
-        }
+        const double sq = (double)v[k] * (double)v[k];
         colacc[k] += sq;
         rowp2[k & 1] += sq;
       }
@@ -268,7 +275,8 @@ __global__ void __launch_bounds__(kFactorThreads, 2) factor_partials_kernel(Devi
     if (T.n == 1) {
       factor_vector(P, it, T);
     } else if ((T.n & 3) == 0 && (reinterpret_cast<uintptr_t>(T.grad) & 15) == 0) {
-      factor_tile_async(P, it, T, F);
+      if (it.b1 - it.b0 == kStripCols) factor_tile_async<true>(P, it, T, F);
+      else factor_tile_async<false>(P, it, T, F);
     } else {
       factor_tile<false>(P, it, T, F.colbuf);
     }
