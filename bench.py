@@ -190,8 +190,12 @@ def build_optimizer(params, feature_set, mode, world, strategy="range", hp=None)
                 return ShardedVeLO(params, mode=mode, check_errors=False, gather=gather,
                                    strategy=strategy, **hp)
             except Exception as e:  # noqa: BLE001
+                if "LOPT_GATHER" in os.environ:
+                    raise   # an explicitly requested exchange is not substituted
                 print(f"bench: p2p gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
-                return ShardedVeLO(params, mode=mode, check_errors=False, strategy=strategy, **hp)
+                opt = ShardedVeLO(params, mode=mode, check_errors=False, strategy=strategy, **hp)
+                opt.gather_fallback = f"p2p unavailable: {e}"[:200]
+                return opt
         from paper_2506_10315_b200.velo import VeLO_CUDA
 
         return VeLO_CUDA(params, mode=mode, check_errors=False, **hp)
@@ -203,9 +207,13 @@ def build_optimizer(params, feature_set, mode, world, strategy="range", hp=None)
                                            check_errors=False, gather=gather, strategy=strategy,
                                            **hp)
         except Exception as e:  # noqa: BLE001
+            if "LOPT_GATHER" in os.environ:
+                raise   # an explicitly requested exchange is not substituted
             print(f"bench: p2p gather unavailable ({e}); NCCL all-gather", file=sys.stderr)
-            return ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
-                                           check_errors=False, strategy=strategy, **hp)
+            opt = ShardedLearnedOptimizer(params, feature_set=feature_set, mode=mode,
+                                          check_errors=False, strategy=strategy, **hp)
+            opt.gather_fallback = f"p2p unavailable: {e}"[:200]
+            return opt
     from paper_2506_10315_b200 import LearnedOptimizer
 
     return LearnedOptimizer(params, feature_set=feature_set, mode=mode, check_errors=False, **hp)
@@ -648,6 +656,7 @@ def main():
     hp = workload_hparams(args.workload)
     opt = build_optimizer(params, args.feature_set, args.mode, world, args.strategy, hp)
     gather_used = getattr(opt, "gather", "nccl")
+    gather_fallback = getattr(opt, "gather_fallback", None)
     clk = ClockSampler(torch.cuda.current_device())
     clk.__enter__()   # sampled through the timed steps, the phase pass and the e2e run
     ms, phases, launches = time_device(opt, params, grads, args.steps, args.warmup, world)
@@ -823,6 +832,7 @@ def main():
             "scaling": "strong" if world > 1 else "none", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "mode": args.mode, "param_exchange": gather_used if world > 1 else None,
+            "param_exchange_fallback": gather_fallback,
             "config": bench_config(args, hp, n_tensors, n_params, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "velo": velo,
             "context": adam, "mnist_mlp": small, "gpt2_medium_velo": cfg5,
