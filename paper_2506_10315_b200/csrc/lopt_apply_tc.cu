@@ -1086,7 +1086,7 @@ __device__ __forceinline__ void pair_producer_loop(const DevicePlan &P, PairSmem
   }
 }
 
-template <int KIND>
+template <int KIND, bool W3C>
 #ifdef LOPT_APPLY_MAXNREG
 #define LOPT_PAIR_BOUNDS __maxnreg__(LOPT_APPLY_MAXNREG)   // leaves registers for a co-resident kernel
 #else
@@ -1437,7 +1437,16 @@ __global__ void LOPT_PAIR_BOUNDS apply_pair_kernel(DevicePlan P) {
         de[0] = make_float2(__uint_as_float(l0[0]), __uint_as_float(l0[1]));
         de[1] = make_float2(__uint_as_float(l1[0]), __uint_as_float(l1[1]));
         dd[0] = dd[1] = make_float2(0.0f, 0.0f);
-        const float4 *w3 = reinterpret_cast<const float4 *>(im.w3h);
+        if (W3C) {
+          // w3 from the launch parameter (uniform registers) lacks the
+          // tensor's 2^s2: run the chains 2^-s2 down and scale the sum back
+          // up -- powers of two, so every rounding is the image path's
+          const float sdn = im.s2_down;
+          de[0] = fmul2(de[0], make_float2(sdn, sdn));
+          de[1] = fmul2(de[1], make_float2(sdn, sdn));
+        }
+        const float4 *w3 = W3C ? reinterpret_cast<const float4 *>(&P.w3c[0][0])
+                               : reinterpret_cast<const float4 *>(im.w3h);
 #pragma unroll
         for (int half = 0; half < 2; half++) {
           if (half == 1) {
@@ -1456,6 +1465,14 @@ __global__ void LOPT_PAIR_BOUNDS apply_pair_kernel(DevicePlan P) {
             ho = fabsf(__uint_as_float(h1[2 * q + 1]));
             de[1] = ffma2(make_float2(he, he), wd, de[1]);
             dd[1] = ffma2(make_float2(ho, ho), wm, dd[1]);
+          }
+        }
+        if (W3C) {
+          const float sup = im.s2_up;
+#pragma unroll
+          for (int k = 0; k < 2; k++) {
+            de[k] = fmul2(de[k], make_float2(sup, sup));
+            dd[k] = fmul2(dd[k], make_float2(sup, sup));
           }
         }
       }
@@ -1563,13 +1580,25 @@ void launch_tc_apply(const DevicePlan &P0, cudaStream_t s) {
     const size_t smem = sizeof(PairSmem) + 1024;
     const int pgrid = P.apply_grid;   // the grid prep balanced the ranges for
     if (P.kind == LOPT_SMALL_FC_LOPT) {
-      cudaFuncSetAttribute(apply_pair_kernel<LOPT_SMALL_FC_LOPT>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      apply_pair_kernel<LOPT_SMALL_FC_LOPT><<<pgrid, kPThreads, smem, s>>>(P);
+      if (P.w3c_on) {
+        cudaFuncSetAttribute(apply_pair_kernel<LOPT_SMALL_FC_LOPT, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        apply_pair_kernel<LOPT_SMALL_FC_LOPT, true><<<pgrid, kPThreads, smem, s>>>(P);
+      } else {
+        cudaFuncSetAttribute(apply_pair_kernel<LOPT_SMALL_FC_LOPT, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        apply_pair_kernel<LOPT_SMALL_FC_LOPT, false><<<pgrid, kPThreads, smem, s>>>(P);
+      }
     } else {
-      cudaFuncSetAttribute(apply_pair_kernel<LOPT_VELO_MLP>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      apply_pair_kernel<LOPT_VELO_MLP><<<pgrid, kPThreads, smem, s>>>(P);
+      if (P.w3c_on) {
+        cudaFuncSetAttribute(apply_pair_kernel<LOPT_VELO_MLP, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        apply_pair_kernel<LOPT_VELO_MLP, true><<<pgrid, kPThreads, smem, s>>>(P);
+      } else {
+        cudaFuncSetAttribute(apply_pair_kernel<LOPT_VELO_MLP, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        apply_pair_kernel<LOPT_VELO_MLP, false><<<pgrid, kPThreads, smem, s>>>(P);
+      }
     }
     return;
   }

@@ -129,6 +129,12 @@ struct lopt_plan {
   int64_t ev_step = 0;                 // steps recorded so far
   cudaGraphNode_t ev_node[5] = {};
   bool graph_ev = false;
+  // layer 3 of a single-weight-set plan, kept on the host for the pair
+  // kernel's launch parameter (DevicePlan::w3c); a plan whose weights were
+  // exposed through lopt_weights_ptr (device-side writes) reads them from the
+  // operand images instead
+  float w3c[16][4] = {};
+  bool w3_known = false, w3_exposed = false;
   void drop_events() {
     for (cudaEvent_t e : phase_ev) cudaEventDestroy(e);
     phase_ev.clear();
@@ -574,14 +580,42 @@ int lopt_set_weights(lopt_plan *p, int32_t slot, const float *packed, int32_t is
   if (slot < 0 || slot >= p->cfg.num_weight_sets) return LOPT_ERR_INVALID;
   const size_t bytes = sizeof(float) * p->dp.weight_stride;
   float *dst = (float *)(p->ws + p->r_weights.off) + (int64_t)slot * p->dp.weight_stride;
-  return check_cuda(cudaMemcpyAsync(dst, packed, bytes,
-                                    is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                    (cudaStream_t)stream));
+  cudaStream_t s = (cudaStream_t)stream;
+  int st;
+  if ((st = check_cuda(cudaMemcpyAsync(dst, packed, bytes,
+                                       is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                       s))))
+    return st;
+  if (p->cfg.num_weight_sets == 1 && p->cfg.mode == LOPT_MODE_FAST) {
+    // w3 (2 x 32 after W1, b1, W2, b2) as the launch parameter, halved
+    const int64_t off = 32 * (int64_t)d_feat(p->cfg.feature_set) + 32 + 32 * 32 + 32;
+    float w3[64];
+    if (is_device) {
+      if ((st = check_cuda(cudaMemcpyAsync(w3, packed + off, sizeof(w3), cudaMemcpyDeviceToHost, s))) ||
+          (st = check_cuda(cudaStreamSynchronize(s))))
+        return st;
+    } else {
+      memcpy(w3, packed + off, sizeof(w3));
+    }
+    float c[16][4];
+    for (int out = 0; out < 2; out++)
+      for (int o = 0; o < 32; o++) c[o >> 1][2 * (o & 1) + out] = w3[out * 32 + o] * 0.5f;
+    if (!p->w3_known || memcmp(c, p->w3c, sizeof(c)) != 0) {
+      memcpy(p->w3c, c, sizeof(c));
+      p->w3_known = true;
+      p->drop_graph();   // the captured apply launch holds the old parameter
+    }
+  }
+  return LOPT_OK;
 }
 
 int lopt_weights_ptr(lopt_plan *p, int32_t slot, float **dev_ptr) {
   if (!p || !p->ws || !dev_ptr || slot < 0 || slot >= p->cfg.num_weight_sets)
     return LOPT_ERR_INVALID;
+  if (!p->w3_exposed) {
+    p->w3_exposed = true;   // device-side writes: layer 3 from the operand images
+    p->drop_graph();
+  }
   *dev_ptr = (float *)(p->ws + p->r_weights.off) + (int64_t)slot * p->dp.weight_stride;
   return LOPT_OK;
 }
@@ -654,7 +688,11 @@ int lopt_apply(lopt_plan *p, void *stream) {
   if (!p || !p->ws) return LOPT_ERR_INVALID;
   cudaStream_t s = (cudaStream_t)stream;
   if (p->cfg.mode == LOPT_MODE_FAST) {
-    launch_fast_apply(p->dp, s);   // prep + persistent tensor-core apply
+    DevicePlan P = p->dp;
+    static const bool no_w3c = getenv("LOPT_NO_W3C") != nullptr;   // A/B switch
+    P.w3c_on = !no_w3c && p->w3_known && !p->w3_exposed && !p->velo && p->cfg.num_weight_sets == 1;
+    if (P.w3c_on) memcpy(P.w3c, p->w3c, sizeof(P.w3c));
+    launch_fast_apply(P, s);   // prep + persistent tensor-core apply
     p->launches_last_step += 1 + (p->dp.n_tiles > 0);
   } else {
     launch_strict_apply(p->dp, s);

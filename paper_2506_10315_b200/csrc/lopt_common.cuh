@@ -125,7 +125,11 @@ struct DevicePlan {
   int32_t *pair_range;    // [kMaxApplyCtas + 1]
   int64_t *cta_perf;      // [kMaxApplyCtas x 2], then [kMaxApplyCtas] f64 smoothed speeds
   int32_t apply_grid;     // pair-kernel CTAs (min(SMs, n_pairs))
-  int32_t pad_grid;
+  int32_t w3c_on;         // w3c holds the plan's one weight set's layer 3
+  // layer 3 of a single-weight-set plan as a launch parameter, laid out like
+  // PrepImage::w3h without the per-tensor 2^s2: the pair kernel's FFMA2s
+  // take it from uniform registers instead of shared memory
+  float w3c[16][4];
   unsigned char *prep;    // per-tensor PrepImage (B operands, layer-3 weights)
   double *bcsum;          // [count x d_feat] closed-form sums of broadcast features
   int32_t dbg, n_peers;   // dbg: timing experiments only (LOPT_APPLY_DEBUG), 0 in production

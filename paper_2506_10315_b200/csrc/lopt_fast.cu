@@ -213,7 +213,8 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(DevicePlan P) {
   if (threadIdx.x >= 17 && threadIdx.x < 20) img->escale[threadIdx.x] = 0.0f;
   if (threadIdx.x == 0) {
     img->s2_down = sd;
-    img->pad[0] = img->pad[1] = 0.0f;
+    img->s2_up = su;
+    img->pad = 0.0f;
   }
   }   // blockIdx.y == 0
   // broadcast operands: rows r5 r6 r7 rr5 rr6 rr7, columns c5 c6 c7 rc5 rc6 rc7

@@ -49,8 +49,9 @@ struct __align__(128) PrepImage {
   float escale[20];         // normalization scale of the per-element columns (+ clip), float4-read
   float b3[2];
   float sqmr[3];            // sqrt(mean r_i)
-  float s2_down;            // 2^-s2 (already folded into W1; kept for inspection)
-  float pad[2];
+  float s2_down;            // 2^-s2 (already folded into W1)
+  float s2_up;              // 2^s2: scales layer 3's |h2| half when w3 comes from the launch
+  float pad;
 };
 static_assert(offsetof(PrepImage, escale) % 16 == 0, "escale is read as float4");
 static_assert(sizeof(PrepImage) % 16 == 0, "PrepImage must be 16-byte granular");
