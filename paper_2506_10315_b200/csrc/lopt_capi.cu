@@ -879,6 +879,7 @@ int lopt_set_velo(lopt_plan *p, const float *hyper, float *lstm_state, const flo
   for (size_t j = 0; j < p->tensors.size(); j++)
     if (p->tensors[j].weight_slot != (int32_t)j) return LOPT_ERR_INVALID;
   p->velo = true;
+  p->w3_exposed = true;   // the hypernetwork writes the weights on the device
   p->v_hyper = hyper;
   p->v_lstm = lstm_state;
   p->v_bank = bank;
@@ -940,6 +941,12 @@ int lopt_velo_mix(lopt_plan *p, const float *hyper, float *lstm_state, const flo
   if (p->cfg.num_weight_sets != (int32_t)p->tensors.size()) return LOPT_ERR_INVALID;
   for (size_t j = 0; j < p->tensors.size(); j++)
     if (p->tensors[j].weight_slot != (int32_t)j) return LOPT_ERR_INVALID;
+  if (!p->w3_exposed) {
+    // the hypernetwork writes the plan's weights on the device: layer 3 from
+    // the operand images from now on
+    p->w3_exposed = true;
+    p->drop_graph();
+  }
   const int st = launch_velo_mix(p->dp, hyper, lstm_state, bank, loss_feats, hidden, bank_size,
                                  mix_out, (cudaStream_t)stream);
   if (st == LOPT_OK) p->launches_last_step += 1;

@@ -119,3 +119,41 @@ def test_phase_timed_graph_step_equals_plain_step(velo):
                 opt.phase_events = None
     for a, b in zip(runs[0][0], runs[1][0]):
         assert torch.equal(a.detach(), b.detach())
+
+
+def test_new_weights_reach_the_launch_parameter_layer3():
+    """A single-weight-set fast plan takes layer 3 from the launch parameter
+    (DevicePlan::w3c): replacing the weights between steps (lopt_set_weights,
+    host or device source) must reach it -- the fast step tracks the strict
+    step (which reads the weights from device memory) after the switch."""
+    import torch
+
+    import paper_2506_10315_b200 as P
+
+    rng = np.random.default_rng(21)
+    init = [np.asarray(rng.standard_normal(s) * 0.05, F32) for s in SHAPES]
+    wa = P.random_weights(39, seed=1)
+    wb = P.random_weights(39, seed=2, scale=0.35)
+    runs = []
+    for mode in ("fast", "strict"):
+        ps = [torch.nn.Parameter(torch.from_numpy(x.copy()).cuda()) for x in init]
+        runs.append((ps, P.LearnedOptimizer(ps, mode=mode, weights=wa)))
+    for k in range(4):
+        gs = [np.asarray(rng.standard_normal(s) * 1e-2, F32) for s in SHAPES]
+        for ps, opt in runs:
+            for p, g in zip(ps, gs):
+                p.grad = torch.from_numpy(g).cuda()
+            if k == 2:
+                for plan in opt.plans():
+                    if opt.mode == "fast":
+                        # device-resident source: the plan reads w3 back
+                        dev = torch.from_numpy(wb.packed()).cuda()
+                        P._lib.check(plan.L.lopt_set_weights(plan.h, 0, dev.data_ptr(), 1, 0))
+                        torch.cuda.synchronize()
+                    else:
+                        plan.set_weights(0, wb)
+            opt.step()
+    torch.cuda.synchronize()
+    for a, b in zip(runs[0][0], runs[1][0]):
+        x, y = a.detach().cpu().numpy(), b.detach().cpu().numpy()
+        assert np.max(np.abs(x - y) / (1.0 + np.abs(y))) < 1e-5
