@@ -19,6 +19,7 @@ void launch_factor_partials(const DevicePlan &P, cudaStream_t s);
 void launch_factor_reduce(const DevicePlan &P, int64_t max_mn, cudaStream_t s);
 void launch_factor_finalize(const DevicePlan &P, int64_t max_mn, cudaStream_t s);
 void launch_factor_means(const DevicePlan &P, cudaStream_t s);
+void launch_factor_reduce_finalize(const DevicePlan &P, cudaStream_t s);
 void launch_strict_stats(const DevicePlan &P, cudaStream_t s);
 void launch_stats_reduce(const DevicePlan &P, cudaStream_t s);
 void launch_strict_apply(const DevicePlan &P, cudaStream_t s);
@@ -761,8 +762,22 @@ int lopt_step(lopt_plan *p, const lopt_step_args *args, void *stream) {
   };
   if (args && (st = lopt_set_step_args(p, args, stream))) return st;
   if ((st = mark(0))) return st;
-  if ((st = lopt_factor_partials(p, stream))) return st;
-  if ((st = lopt_factor_finalize(p, stream))) return st;
+  if (p->cfg.state_advanced) {
+    if ((st = lopt_factor_partials(p, stream))) return st;
+    if ((st = lopt_factor_finalize(p, stream))) return st;
+  } else {
+    // one device: no merge between the reduce and the finalize -- one kernel
+    if (!p->begun) {
+      begin_step_kernel<<<begin_blocks(p), 256, 0, s>>>(p->dp, StepScalars{}, 0);
+      p->launches_last_step = 1;
+    }
+    p->begun = false;
+    launch_factor_partials(p->dp, s);
+    launch_factor_reduce_finalize(p->dp, s);
+    launch_factor_means(p->dp, s);
+    p->launches_last_step += 3;
+    if ((st = check_launch())) return st;
+  }
   if ((st = mark(1))) return st;
   if ((st = lopt_feature_stats(p, stream))) return st;
   if ((st = mark(2))) return st;

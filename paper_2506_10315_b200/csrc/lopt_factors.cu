@@ -301,7 +301,11 @@ __device__ __forceinline__ int tensor_of(const int64_t *prefix, int count, int64
 // rows (one thread each, over the <= a few strips) and columns (one warp
 // each: lanes take every 32nd row block, then a fixed shuffle tree -- the
 // GPT-2 embedding has 197 row blocks per column).
-__global__ void factor_reduce_kernel(DevicePlan P) {
+__device__ __forceinline__ void finalize_one(const DevicePlan &P, int jt, const TensorDesc &T,
+                                             bool is_row, int64_t i, double sum);
+// FIN: each row / column sum is finalized by the thread that forms it
+template <bool FIN>
+__global__ void factor_reduce_kernel_t(DevicePlan P) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= P.red_total) return;   // whole warps: every segment is a multiple of 32
   const int j = tensor_of(P.red_prefix, P.count, idx);
@@ -312,6 +316,7 @@ __global__ void factor_reduce_kernel(DevicePlan P) {
       double s = 0.0;
       for (int k = 0; k < T.nstrips; k++) s += T.rowpart[(int64_t)k * T.m + local];
       T.rowsum[local] = s;
+      if (FIN) finalize_one(P, j, T, true, local, s);
     }
     return;
   }
@@ -321,6 +326,7 @@ __global__ void factor_reduce_kernel(DevicePlan P) {
       double s = 0.0;
       for (int k = 0; k < T.nrowblocks; k++) s += T.colpart[(int64_t)k * T.n + b];
       T.colsum[b] = s;
+      if (FIN) finalize_one(P, j, T, false, b, s);
     }
     return;
   }
@@ -330,20 +336,20 @@ __global__ void factor_reduce_kernel(DevicePlan P) {
   for (int k = lane; k < T.nrowblocks; k += 32) s += T.colpart[(int64_t)k * T.n + b];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-  if (lane == 0) T.colsum[b] = s;
+  if (lane == 0) {
+    T.colsum[b] = s;
+    if (FIN) finalize_one(P, j, T, false, b, s);
+  }
 }
 
 // state.py:108-113: mean = f32(sum / len), r' = b*r + (1-b)*mean in f32; then
 // the row/column tables the features read: {x5', x6', x7', 1/sqrt(x'+eps) x3}.
 // With state_advanced the factors are taken as given.
-__global__ void factor_finalize_kernel(DevicePlan P) {
-  const int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gidx >= P.fin_total) return;
-  const int jt = tensor_of(P.fin_prefix, P.count, gidx);
-  const TensorDesc &T = P.tensors[jt];
-  const int64_t idx = gidx - P.fin_prefix[jt];
-  const bool is_row = idx < T.m;
-  const int64_t i = is_row ? idx : idx - T.m;
+// One row (or column) i of tensor jt: the EMA of r' (c') from this step's f64
+// sum of g^2 (state.py:108-113), or the already advanced factors, and the
+// row (column) table entries the per-element features read.
+__device__ __forceinline__ void finalize_one(const DevicePlan &P, int jt, const TensorDesc &T,
+                                             bool is_row, int64_t i, double sum) {
   const int64_t len = is_row ? T.m : T.n;
   float *fac = is_row ? T.r : T.c;
   float *tab = (is_row ? T.rowtab : T.coltab) + i * kRowTab;
@@ -352,7 +358,6 @@ __global__ void factor_finalize_kernel(DevicePlan P) {
 #pragma unroll
     for (int k = 0; k < 3; k++) x[k] = fac[k * len + i];
   } else {
-    const double sum = is_row ? T.rowsum[i] : T.colsum[i];
     if (*P.grad_flag != 0.0) {
       // a non-finite gradient on any rank (the flag is all-reduced with the
       // sums): abort before any state is written (optim.py:160-165)
@@ -374,6 +379,18 @@ __global__ void factor_finalize_kernel(DevicePlan P) {
   float4 *t4 = reinterpret_cast<float4 *>(tab);
   t4[0] = make_float4(x[0], x[1], x[2], rsqrt_strict(x[0]));
   t4[1] = make_float4(rsqrt_strict(x[1]), rsqrt_strict(x[2]), 0.f, 0.f);
+}
+
+__global__ void factor_finalize_kernel(DevicePlan P) {
+  const int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gidx >= P.fin_total) return;
+  const int jt = tensor_of(P.fin_prefix, P.count, gidx);
+  const TensorDesc &T = P.tensors[jt];
+  const int64_t idx = gidx - P.fin_prefix[jt];
+  const bool is_row = idx < T.m;
+  const int64_t i = is_row ? idx : idx - T.m;
+  const double sum = P.state_advanced ? 0.0 : (is_row ? T.rowsum[i] : T.colsum[i]);
+  finalize_one(P, jt, T, is_row, i, sum);
 }
 
 // features.py:133-135: mr_i = f32(mean_f64(r_i')).  One CTA per tensor,
@@ -471,7 +488,14 @@ void launch_factor_partials(const DevicePlan &P, cudaStream_t s) {
 void launch_factor_reduce(const DevicePlan &P, int64_t max_mn, cudaStream_t s) {
   (void)max_mn;
   if (P.red_total > 0)
-    factor_reduce_kernel<<<(unsigned)((P.red_total + 255) / 256), 256, 0, s>>>(P);
+    factor_reduce_kernel_t<false><<<(unsigned)((P.red_total + 255) / 256), 256, 0, s>>>(P);
+}
+
+// single-device step: the row / column sums finalized by the threads that
+// reduce them (no cross-rank merge between the two)
+void launch_factor_reduce_finalize(const DevicePlan &P, cudaStream_t s) {
+  if (P.red_total > 0)
+    factor_reduce_kernel_t<true><<<(unsigned)((P.red_total + 255) / 256), 256, 0, s>>>(P);
 }
 
 void launch_factor_finalize(const DevicePlan &P, int64_t max_mn, cudaStream_t s) {
