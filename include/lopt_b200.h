@@ -116,11 +116,15 @@ int lopt_bind_workspace(lopt_plan *plan, void *dev_ptr, size_t bytes, void *stre
  * without changing shapes or ranges; re-uploads the descriptor table. */
 int lopt_rebind_tensors(lopt_plan *plan, const lopt_tensor *tensors, int32_t count, void *stream);
 /* MLP weights for set `slot`, device or host pointer to the packed layout
- * w1 (h1 x d) | b1 (h1) | w2 (h2 x h1) | b2 (h2) | w3 (2 x h2) | b3 (2). */
+ * w1 (h1 x d) | b1 (h1) | w2 (h2 x h1) | b2 (h2) | w3 (2 x h2) | b3 (2).
+ * A fast plan with one weight set also keeps w3 on the host for the apply
+ * kernel's launch parameter (a device source is read back synchronously on
+ * `stream`). */
 int lopt_set_weights(lopt_plan *plan, int32_t slot, const float *packed, int32_t is_device,
                      void *stream);
 /* Device pointer to the per-set packed weights (for weights produced on the GPU,
- * e.g. the VeLO mixing kernel). */
+ * e.g. the VeLO mixing kernel).  From the first call on, the plan reads layer 3
+ * from device memory every step (writes through the pointer take effect). */
 int lopt_weights_ptr(lopt_plan *plan, int32_t slot, float **dev_ptr);
 int lopt_set_step_args(lopt_plan *plan, const lopt_step_args *args, void *stream);
 /* Element count behind each tensor's feature statistics, used by the apply
