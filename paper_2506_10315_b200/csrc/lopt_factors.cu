@@ -120,7 +120,10 @@ __device__ void factor_tile(const DevicePlan &P, const FactorItem &it, const Ten
 // groups, so a lane waits on its own copy groups (no cross-lane sync) while
 // the next row pair is already in flight -- twice the bytes in flight of the
 // register-staged loop without registers to hold them.
-constexpr int kFactorBufs = 2;
+#ifndef LOPT_FACTOR_BUFS
+#define LOPT_FACTOR_BUFS 2   // row-pair buffers per warp (prefetch distance + 1)
+#endif
+constexpr int kFactorBufs = LOPT_FACTOR_BUFS;
 struct FactorSmem {
   double colbuf[kFactorWarps][kStripCols];
   float4 rows[kFactorWarps][kFactorBufs][2][kStripCols / 4];
@@ -169,11 +172,14 @@ __device__ void factor_tile_async(const DevicePlan &P, const FactorItem &it, con
     cp_async_commit();
   };
   bool bad = false;
-  if (npairs > 0) issue(0);
+  constexpr int kAhead = kFactorBufs - 1;
+#pragma unroll
+  for (int q = 0; q < kAhead; q++)
+    if (q < npairs) issue(q);
   for (int q = 0; q < npairs; q++) {
-    if (q + 1 < npairs) {
-      issue(q + 1);
-      cp_async_wait<1>();
+    if (q + kAhead < npairs) {
+      issue(q + kAhead);
+      cp_async_wait<kAhead>();
     } else {
       cp_async_wait<0>();
     }
