@@ -10,7 +10,19 @@
 // fp16 terms and each product is x_hi*W_hi + x_lo*W_hi + x_hi*W_lo with f32
 // accumulation (see PrepImage in lopt_fast.cuh for the operand layout).
 //
-// Structure: a warp-specialized persistent kernel, one CTA per SM, that
+// Default kernel (apply_pair_kernel, LOPT_APPLY_VARIANT 3): persistent, one
+// CTA per SM; three producer warps stage tile *pairs* (two 128-element tiles
+// of one tensor) into a ring with TMA bulk copies, and three math warpgroups
+// each carry every third pair through all stages in their own two TMEM slots:
+// features -> E/B operands -> layer-1 MMAs -> ReLU + fp16 split -> layer-2
+// MMAs -> layer 3, update, stores.  Each CTA's pair range comes from prep's
+// balance of the previous launch's per-CTA speeds (pair_range / cta_perf);
+// a single-weight-set plan takes layer 3's weights from the launch parameter
+// (uniform registers, DevicePlan::w3c).  DESIGN.md section 3 has the details
+// and the variants measured.
+//
+// The older role-specialized kernel (apply_tc_kernel, LOPT_APPLY_VARIANT 1),
+// kept for A/B: a warp-specialized persistent kernel, one CTA per SM, that
 // streams the CTA's contiguous range of tiles through a pipeline:
 //
 //   producer warps --TMA bulk copies-->  smem ring of kRing tile slots
@@ -33,7 +45,7 @@
 //
 // Tiles of tensors with n % 128 == 0 are (row, 128-column block) pairs in
 // column-block-major order, so consecutive tiles share their column-table
-// entries (kept in WG_A's registers); other tensors use flat 128-element tiles.
+// entries; other tensors use flat 128-element tiles.
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
